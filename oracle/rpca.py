@@ -1,0 +1,104 @@
+"""Host solvers around FRSVT (fp64). TEST INFRASTRUCTURE ONLY.
+
+rpca_ialm       : inexact ALM Robust PCA ("using an inexact
+                  augmented Lagrange multiplier method [18] (iALM)"), textbook
+                  order and constants of SPEC S:449/S:471 (reading Z9):
+                    lambda = 1/sqrt(max(m,n))
+                    mu_0 = 1.25/||D||_2, mu_bar = 1e7 mu_0, rho (BASELINE)
+                    Y_0 = D / max(||D||_2, ||D||_inf / lambda), L_0 = E_0 = 0
+                    loop: E <- S_{lambda/mu}(D - L + Y/mu)
+                          L <- FRSVT_{1/mu}(D - E + Y/mu)   (carry Q~ if RP)
+                          Y <- Y + mu (D - L - E);  mu <- min(rho mu, mu_bar)
+                  fixed iteration count, no early stop (BASELINE configs).
+                  Pinned by dual feasibility ||Y_k||_2 <= 1 with the exact
+                  backend, E -> 0 on uncorrupted low-rank D and
+                  exact-vs-FRSVT backend agreement. Absolute recovery
+                  errors at BASELINE sizes: parity unpinned (no paper number;
+                  compared only against ground truth and the GPU path).
+reweighted_wsvt : BASELINE c4 "20 proximal iterations" read as the reweighted
+                  prox X_{t+1} = WSVT_{w(t)}(A) (reading Z13): call 0 uses
+                  w_i = C/(sigma_i + eps) of its own sigma, call t >= 1 uses
+                  w_i = C/(d_i^{(t-1)} + eps) of the previous shrunk values
+                  (padded with zeros). Pinned on diagonal inputs by the scalar
+                  recurrence sigma <- max(sigma_A - C/(sigma + eps), 0).
+"""
+import numpy as np
+
+from .frsvt import frsvt
+from .linalg import norm2_power
+from .svt import soft_shrink, svt_exact
+
+
+def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
+              mu_max_factor=1e7, norm2=None, L0=None, backend="frsvt",
+              record_states=False):
+    """Returns dict with L, E, Y, mu and per-iteration history.
+
+    omega_fn(k) -> Omega (n x l) for iteration k (call index k).
+    record_states: keep (E_{k+1}, operand A_k, mu_k, carry_k, Omega_k) of
+    every iteration for teacher-forced parity.
+    """
+    D = np.asarray(D, dtype=np.float64)
+    m, n = D.shape
+    if lam is None:
+        lam = 1.0 / np.sqrt(max(m, n))
+    if norm2 is None:
+        norm2 = norm2_power(D)
+    if mu0 is None:
+        mu0 = 1.25 / norm2
+    mu = mu0
+    mu_bar = mu_max_factor * mu0
+    Y = D / max(norm2, np.max(np.abs(D)) / lam)
+    L = np.zeros_like(D)
+    E = np.zeros_like(D)
+    carry = None
+    hist = dict(r=[], s=[], resid=[], nrmse=[], mu=[])
+    states = []
+    nD = np.linalg.norm(D)
+    for k in range(n_iter):
+        E = soft_shrink(D - L + Y / mu, lam / mu)
+        Aop = D - E + Y / mu
+        if backend == "exact":
+            L, _, r = svt_exact(Aop, 1.0 / mu)
+            s = min(m, n)
+            new_carry = None
+        else:
+            Om = omega_fn(k)
+            if record_states:
+                states.append(dict(E=E.copy(), A=Aop.copy(), mu=mu,
+                                   carry=None if carry is None else carry.copy(),
+                                   Omega=np.array(Om, dtype=np.float64)))
+            res = frsvt(Aop, Om, l, q, tau=1.0 / mu, carry=carry, rp=rp)
+            L, r, s, new_carry = res.X, res.r, res.s, res.carry
+        carry = new_carry if rp else None
+        Y = Y + mu * (D - L - E)
+        hist["r"].append(r)
+        hist["s"].append(s)
+        hist["resid"].append(np.linalg.norm(D - L - E) / nD)
+        hist["mu"].append(mu)
+        if L0 is not None:
+            hist["nrmse"].append(np.linalg.norm(L - L0) / np.linalg.norm(L0))
+        mu = min(rho * mu, mu_bar)
+    return dict(L=L, E=E, Y=Y, mu=mu, mu0=mu0, lam=lam, norm2=norm2, hist=hist,
+                states=states, carry=carry)
+
+
+def reweighted_wsvt(A, n_calls, l, q, C, eps, omega_fn, rp=True):
+    """Reweighted weighted-SVT sequence of BASELINE c4 (reading Z13).
+    Returns the list of FrsvtResult, one per call."""
+    A = np.asarray(A, dtype=np.float64)
+    out = []
+    carry = None
+    d_prev = None
+    for t in range(n_calls):
+        Om = omega_fn(t)
+        if d_prev is None:
+            res = frsvt(A, Om, l, q, C=C, eps=eps, carry=carry, rp=rp)
+        else:
+            dp = np.zeros(l)
+            dp[: min(l, len(d_prev))] = d_prev[:l]
+            res = frsvt(A, Om, l, q, w=C / (dp + eps), carry=carry, rp=rp)
+        out.append(res)
+        carry = res.carry if rp else None
+        d_prev = res.d
+    return out
