@@ -1,0 +1,185 @@
+/*
+ * frsvt.h — C ABI of libfrsvt, the B200 (sm_100a) hot path of
+ * "Fast Randomized Singular Value Thresholding for Low-rank Optimization"
+ * (Oh, Matsushita, Tai, Kweon; arXiv 1509.00296). Citations "P:n" are lines of
+ * the paper text; "S:n" lines of SPEC.md; readings Zn / Rn are
+ * listed in DESIGN.md.
+ *
+ * Layout. Every matrix is COLUMN-MAJOR with an explicit leading dimension.
+ * A matrix argument is a DEVICE pointer unless the comment says "host".
+ * Element type is double (FRSVT_F64) or float (FRSVT_F32), fixed per handle.
+ * A multi-GPU run row-shards every m-row operand: rank k owns rows
+ * [row0, row0 + m_local) of the m_global x n matrix.
+ *
+ * Ownership. The caller owns A, X, D, E, the ALM operand and L and never
+ * hands them over; the library never frees or reallocates them. The handle
+ * owns Omega, every workspace, the carried basis Q~ and the NCCL communicator.
+ * All handle memory is allocated in frsvt_create; no apply/step call
+ * allocates, so one call is CUDA-graph capturable.
+ *
+ * Asynchrony. Work is enqueued on the handle's stream; calls return before it
+ * completes unless a host output (info, rel_resid, get_* hooks) is requested,
+ * which synchronises that stream. One handle per host thread.
+ *
+ * Errors. Arguments are validated before anything is enqueued; an invalid
+ * call returns FRSVT_EINVAL and enqueues nothing. Numerical rank deficiency
+ * is NOT an error: it is absorbed by truncation (info.s < l), the rank reveal
+ * of QR-CP. A non-finite Gram diagonal sets FRSVT_FLAG_NONFINITE
+ * (status FRSVT_ENONFINITE at the next synchronising call); a Jacobi solve that
+ * hits its sweep cap sets FRSVT_FLAG_NOCONV (X is still written). CUDA / NCCL
+ * failures map to FRSVT_ECUDA / FRSVT_ENCCL. No C++ exception crosses the ABI.
+ */
+#ifndef FRSVT_H
+#define FRSVT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRSVT_LMAX 128  /* largest sketch width l supported */
+
+typedef enum {
+  FRSVT_OK = 0,
+  FRSVT_EINVAL = 1,
+  FRSVT_ENOCONV = 2,
+  FRSVT_ECUDA = 3,
+  FRSVT_ENCCL = 4,
+  FRSVT_ENONFINITE = 5,
+  FRSVT_ENOMEM = 6
+} frsvt_status;
+
+typedef enum { FRSVT_F32 = 0, FRSVT_F64 = 1 } frsvt_dtype;
+
+/* info.flags bits */
+#define FRSVT_FLAG_NONFINITE 1
+#define FRSVT_FLAG_NOCONV 2
+#define FRSVT_FLAG_NONMONOTONE_W 4
+
+typedef struct {
+  int32_t dtype;            /* frsvt_dtype */
+  int64_t m_local;          /* rows held by this rank (>= 1) */
+  int64_t n;                /* columns (>= 1) */
+  int64_t m_global;         /* rows of the whole matrix (== m_local if nranks == 1) */
+  int64_t row0;             /* first global row of this rank */
+  int32_t l;                /* sketch width l = k + p (BASELINE "k", reading Z1), 1 <= l <= min(m_global, n, FRSVT_LMAX) */
+  int32_t q;                /* power iterations eta >= 0 (reading Z2) */
+  int32_t range_propagation;/* 1: carry Q~ between calls and draw only p = l - r fresh columns */
+  uint64_t seed;            /* Omega of call c = Philox4x32-10(key = seed, stream 1000 + c) + Box-Muller */
+  int32_t nranks;           /* 1 for a single GPU */
+  int32_t rank;             /* 0 .. nranks-1 */
+  const unsigned char* nccl_id; /* host, 128 bytes from frsvt_get_unique_id on rank 0; NULL if nranks == 1 */
+} frsvt_config;
+
+/* Host-side report of one call (filling it synchronises the stream). */
+typedef struct {
+  int32_t s;                /* basis width after rank reveal (s = min(l, rank)) */
+  int32_t r;                /* kept rank #{d_i > 0} = width of the carried Q~ */
+  int32_t flags;            /* FRSVT_FLAG_* */
+  int32_t sweeps;           /* Jacobi sweeps of the small SVD */
+  int64_t calls;            /* Omega call counter after this call */
+  double sigma[FRSVT_LMAX]; /* singular values of B = Q^T A, descending (first s valid) */
+  double d[FRSVT_LMAX];     /* shrunk values max(sigma_i - t_i, 0) */
+  double mu;                /* rpca: mu used by the last step */
+} frsvt_info;
+
+typedef struct frsvt_handle frsvt_handle;
+
+/* 128-byte NCCL unique id (rank 0 only); the caller broadcasts it, e.g. with
+ * torch.distributed, and passes it to frsvt_create on every rank. */
+frsvt_status frsvt_get_unique_id(unsigned char out[128]);
+
+/* Validate cfg, allocate every workspace for width l on the current device,
+ * bind the work to `cuda_stream` (a cudaStream_t, NULL = legacy default),
+ * and initialise NCCL when nranks > 1. *out is NULL on failure. */
+frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_handle** out);
+void frsvt_destroy(frsvt_handle* h);
+const char* frsvt_status_string(frsvt_status s);
+
+/* X <- FRSVT_tau(A): Algorithm 1, Eq. (6), with the
+ * singular value thresholding of Definition 1:
+ *   sketch Y = A Omega (RP: Y = [Q~ | A Omega_p]), q power steps
+ *   Q <- orth(A orth(A^T Q)), B = Q^T A, small SVD of B, shrink, compose.
+ * A: m_local x n, leading dim lda >= m_local. X: m_local x n, ldx >= m_local,
+ * may alias A (every read of A completes before X is written).
+ * tau >= 0 finite. info: host, nullable (non-NULL synchronises). */
+frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau,
+                         void* X, int64_t ldx, frsvt_info* info);
+
+/* Weighted SVT (WNNM's WSVT, footnote 1 P:48): per-index thresholds t_i on
+ * sigma_i sorted descending.
+ *   wmode 0 (explicit)     : t_i = w[i], w host array of l values >= 0
+ *   wmode 1 (reciprocal)   : t_i = C / (sigma_i + eps) on this call's sigma
+ *   wmode 2 (reweighted)   : t_i = C / (d_i^prev + eps), d^prev the shrunk
+ *                            values of the handle's previous call (zeros past
+ *                            its rank); the first call falls back to mode 1.
+ * Non-monotone t is applied mechanically and flagged NONMONOTONE_W. */
+frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda,
+                                  int32_t wmode, const double* w, double C, double eps,
+                                  void* X, int64_t ldx, frsvt_info* info);
+
+/* Inexact-ALM Robust PCA step hosting FRSVT (order and constants of
+ * S:449/S:471, reading Z9), with the stored operand A_k = D - E_{k+1} + Y_k/mu_k
+ * so Y is never materialised (Y_{k+1} = mu_k (A_k - L_{k+1})):
+ *   L_{k+1} = FRSVT_{1/mu_k}(A_k)             (no m x n write of L)
+ *   resid_k = ||D - L_{k+1} - E_{k+1}||_F / ||D||_F
+ *   mu_{k+1} = min(rho mu_k, mu_bar)
+ *   E_{k+2} = S_{lambda/mu_{k+1}}(D - L_{k+1} + Y_{k+1}/mu_{k+1})
+ *   A_{k+1} = D - E_{k+2} + Y_{k+1}/mu_{k+1}
+ * all in ONE fused epilogue pass over D, A, E (reads D, A, E; writes A, E).
+ * iter == 0 first runs the init: ||D||_2 (norm2_D, else a device block power
+ * estimate), ||D||_inf, Y_0 = D / max(||D||_2, ||D||_inf / lambda),
+ * mu_0 (mu0, else 1.25/||D||_2), E_1, A_1. finalize != 0 writes L_{k+1} into
+ * st->L and leaves D, E, A, mu untouched (the textbook state after k+1 steps).
+ * D, E, A, L: m_local x n, leading dim ld. rel_resid: host, nullable (syncs). */
+typedef struct {
+  const void* D;     /* observation */
+  void* E;           /* sparse part; holds E_{k+1} on entry of step k */
+  void* A;           /* ALM operand A_k (library-managed contents) */
+  void* L;           /* low-rank output, written only when finalize != 0 */
+  int64_t ld;
+  double lambda;     /* <= 0 -> 1/sqrt(max(m_global, n)) */
+  double rho;        /* mu growth factor (> 1) */
+  double mu_max_factor; /* mu_bar = mu_max_factor * mu_0 (reading Z9: 1e7) */
+  double norm2_D;    /* > 0 supplied ||D||_2; 0 -> estimated on device at iter 0 */
+  double mu0;        /* > 0 supplied mu_0; 0 -> 1.25 / ||D||_2 */
+  int32_t iter;      /* in/out: k; incremented by every non-finalize step */
+} rpca_state;
+
+frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, double* rel_resid);
+
+/* ---- test / parity hooks (host outputs synchronise) ----------------------- */
+/* Next call uses this n x l Omega (device, leading dim ldo) instead of Philox. */
+frsvt_status frsvt_set_omega(frsvt_handle* h, const void* Omega, int64_t ldo);
+/* Write the handle's Philox Omega of call `call` (n x l) to `out` (device). */
+frsvt_status frsvt_draw_omega(frsvt_handle* h, int64_t call, void* out, int64_t ldo);
+/* Carried basis Q~ (m_local x l, columns >= r zero) and its width r. */
+frsvt_status frsvt_get_carry(frsvt_handle* h, void* Qt, int64_t ldq, int32_t* r);
+frsvt_status frsvt_set_carry(frsvt_handle* h, const void* Qt, int64_t ldq, int32_t r);
+frsvt_status frsvt_reset_carry(frsvt_handle* h);
+/* Set the Omega call counter (the next call draws Omega of call `call`). */
+frsvt_status frsvt_set_call_index(frsvt_handle* h, int64_t call);
+/* Last call's report (synchronises). */
+frsvt_status frsvt_get_info(frsvt_handle* h, frsvt_info* info);
+/* rpca: device mu (host copy) and set it (teacher forcing). */
+frsvt_status rpca_get_mu(frsvt_handle* h, double* mu);
+frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar);
+/* Number of kernels this handle has launched since creation (host counter). */
+int64_t frsvt_kernel_launches(const frsvt_handle* h);
+
+/* Pass profiling: with enable != 0 every kernel that streams the m x n
+ * operand is bracketed by CUDA events on the handle's stream (enabling resets
+ * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,
+ * B), 2 = composition / fused iALM epilogue. Reading synchronises and returns
+ * the summed event time (ms), the launch count and the algorithmic bytes of
+ * those launches (m*n*elem per A pass; X write; 5 m*n*elem for the iALM
+ * epilogue: D, A, E read, A, E written; 3 m*n*elem for a finalize step). */
+frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable);
+frsvt_status frsvt_profile_read(frsvt_handle* h, int32_t kind, double* ms, int64_t* launches, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRSVT_H */

@@ -1,0 +1,231 @@
+"""paper_1509_00296_b200 — B200-native FRSVT (arXiv 1509.00296).
+
+Thin Python binding over libfrsvt.so (C ABI in include/frsvt.h): argument
+marshalling only. Every step of the hot path runs in the library's sm_100a
+kernels; there is no CPU or eager-PyTorch fallback. Importing raises if the
+library is missing, and every call raises on a non-OK status.
+
+PyTorch supplies device memory, the CUDA stream and (for multi-GPU runs) the
+process group used to broadcast the NCCL unique id.
+"""
+import ctypes
+import os
+
+import torch
+
+from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FrsvtConfig, FrsvtInfo, RpcaState,
+                   load_library, status_string)
+
+__all__ = ["Frsvt", "FrsvtError", "lib", "library_path", "colmajor", "W_EXPLICIT",
+           "W_RECIPROCAL", "W_REWEIGHTED"]
+
+W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
+
+lib, library_path = load_library()
+
+
+class FrsvtError(RuntimeError):
+    def __init__(self, fn, st):
+        super().__init__("%s failed: %s (status %d)" % (fn, status_string(lib, st), st))
+        self.status = st
+
+
+def _check(fn, st):
+    if st != 0:
+        raise FrsvtError(fn, st)
+
+
+def colmajor(x):
+    """Column-major copy/view of a 2-D tensor (the library layout)."""
+    if x.stride(0) == 1 and x.stride(1) >= max(1, x.shape[0]):
+        return x
+    return x.t().contiguous().t()
+
+
+def _ld(x, rows, dtype, name):
+    if x.device.type != "cuda":
+        raise ValueError("%s must be a CUDA tensor" % name)
+    if x.dtype != dtype:
+        raise ValueError("%s must be %s, got %s" % (name, dtype, x.dtype))
+    if x.dim() != 2 or x.shape[0] != rows:
+        raise ValueError("%s must have %d rows, got shape %s" % (name, rows, tuple(x.shape)))
+    if x.stride(0) != 1 or x.stride(1) < max(1, rows):
+        raise ValueError("%s must be column-major (stride (1, ld>=rows)), got %s" % (name, x.stride()))
+    return x.stride(1)
+
+
+class Frsvt:
+    """One FRSVT handle: fixed shape (m_local x n), sketch width l, power
+    iterations q, range propagation flag, dtype (torch.float32/float64)."""
+
+    def __init__(self, m, n, l, q=1, rp=True, dtype=torch.float32, seed=0, stream=None,
+                 nranks=1, rank=0, m_global=None, row0=0, nccl_id=None, device=None):
+        if device is not None:
+            torch.cuda.set_device(device)
+        self.m, self.n, self.l, self.q, self.rp = int(m), int(n), int(l), int(q), bool(rp)
+        self.dtype = dtype
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        cfg = FrsvtConfig()
+        cfg.dtype = FRSVT_F32 if dtype == torch.float32 else FRSVT_F64
+        cfg.m_local = self.m
+        cfg.n = self.n
+        cfg.m_global = self.m if m_global is None else int(m_global)
+        cfg.row0 = int(row0)
+        cfg.l = self.l
+        cfg.q = self.q
+        cfg.range_propagation = 1 if rp else 0
+        cfg.seed = int(seed)
+        cfg.nranks = int(nranks)
+        cfg.rank = int(rank)
+        self._id_buf = None
+        if nccl_id is not None:
+            self._id_buf = (ctypes.c_ubyte * 128)(*bytes(nccl_id))
+            cfg.nccl_id = ctypes.cast(self._id_buf, ctypes.POINTER(ctypes.c_ubyte))
+        self._h = ctypes.c_void_p()
+        _check("frsvt_create", lib.frsvt_create(ctypes.byref(cfg), ctypes.c_void_p(self.stream.cuda_stream),
+                                                ctypes.byref(self._h)))
+        self.cfg = cfg
+
+    # -- lifecycle --------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib.frsvt_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def unique_id():
+        buf = (ctypes.c_ubyte * 128)()
+        _check("frsvt_get_unique_id", lib.frsvt_get_unique_id(buf))
+        return bytes(buf)
+
+    # -- operator ---------------------------------------------------------
+    def _out(self, X, like):
+        if X is None:
+            X = torch.empty((self.n, self.m), dtype=self.dtype, device=like.device).t()
+        return X
+
+    def apply(self, A, tau, X=None, info=False):
+        """X = FRSVT_tau(A) (Alg. 1, Eq. 6). Returns X (and FrsvtInfo if info)."""
+        lda = _ld(A, self.m, self.dtype, "A")
+        X = self._out(X, A)
+        ldx = _ld(X, self.m, self.dtype, "X")
+        inf = FrsvtInfo() if info else None
+        _check("frsvt_apply", lib.frsvt_apply(self._h, ctypes.c_void_p(A.data_ptr()), lda, float(tau),
+                                              ctypes.c_void_p(X.data_ptr()), ldx,
+                                              ctypes.byref(inf) if info else None))
+        return (X, inf) if info else X
+
+    def apply_weighted(self, A, mode, w=None, C=0.0, eps=1e-6, X=None, info=False):
+        """Weighted SVT: mode W_EXPLICIT (w, length l), W_RECIPROCAL
+        (C/(sigma+eps)) or W_REWEIGHTED (C/(d_prev+eps))."""
+        lda = _ld(A, self.m, self.dtype, "A")
+        X = self._out(X, A)
+        ldx = _ld(X, self.m, self.dtype, "X")
+        wbuf = None
+        if mode == W_EXPLICIT:
+            if w is None or len(w) < self.l:
+                raise ValueError("explicit weights need l values")
+            wbuf = (ctypes.c_double * self.l)(*[float(v) for v in list(w)[: self.l]])
+        inf = FrsvtInfo() if info else None
+        _check("frsvt_apply_weighted",
+               lib.frsvt_apply_weighted(self._h, ctypes.c_void_p(A.data_ptr()), lda, int(mode), wbuf,
+                                        float(C), float(eps), ctypes.c_void_p(X.data_ptr()), ldx,
+                                        ctypes.byref(inf) if info else None))
+        return (X, inf) if info else X
+
+    def rpca_step(self, state, finalize=False, want_resid=False):
+        """One fused iALM step (rpca_alm_step). `state` is an RpcaState."""
+        res = ctypes.c_double(0.0)
+        _check("rpca_alm_step", lib.rpca_alm_step(self._h, ctypes.byref(state), 1 if finalize else 0,
+                                                  ctypes.byref(res) if want_resid else None))
+        return res.value if want_resid else None
+
+    def rpca_state(self, D, E, A, L=None, lam=0.0, rho=1.5, mu_max_factor=1e7, norm2_D=0.0, mu0=0.0):
+        ld = _ld(D, self.m, self.dtype, "D")
+        for t, nm in ((E, "E"), (A, "A")) + (((L, "L"),) if L is not None else ()):
+            if _ld(t, self.m, self.dtype, nm) != ld:
+                raise ValueError("D, E, A, L must share one leading dimension")
+        st = RpcaState()
+        st.D = D.data_ptr()
+        st.E = E.data_ptr()
+        st.A = A.data_ptr()
+        st.L = L.data_ptr() if L is not None else None
+        st.ld = ld
+        st.lambda_ = float(lam)
+        st.rho = float(rho)
+        st.mu_max_factor = float(mu_max_factor)
+        st.norm2_D = float(norm2_D)
+        st.mu0 = float(mu0)
+        st.iter = 0
+        st._keep = (D, E, A, L)
+        return st
+
+    # -- hooks ------------------------------------------------------------
+    def set_omega(self, Om):
+        ld = _ld(Om, self.n, self.dtype, "Omega")
+        _check("frsvt_set_omega", lib.frsvt_set_omega(self._h, ctypes.c_void_p(Om.data_ptr()), ld))
+
+    def draw_omega(self, call):
+        out = torch.empty((self.l, self.n), dtype=self.dtype, device="cuda").t()
+        _check("frsvt_draw_omega", lib.frsvt_draw_omega(self._h, int(call), ctypes.c_void_p(out.data_ptr()),
+                                                        self.n))
+        return out
+
+    def get_carry(self):
+        out = torch.empty((self.l, self.m), dtype=self.dtype, device="cuda").t()
+        r = ctypes.c_int32(0)
+        _check("frsvt_get_carry", lib.frsvt_get_carry(self._h, ctypes.c_void_p(out.data_ptr()), self.m,
+                                                      ctypes.byref(r)))
+        return out[:, : r.value], r.value
+
+    def set_carry(self, Qt):
+        r = 0 if Qt is None else Qt.shape[1]
+        if r:
+            Qt = colmajor(Qt.to(self.dtype).cuda())
+            ld = _ld(Qt, self.m, self.dtype, "carry")
+            ptr = ctypes.c_void_p(Qt.data_ptr())
+        else:
+            ld, ptr = self.m, None
+        _check("frsvt_set_carry", lib.frsvt_set_carry(self._h, ptr, ld, r))
+
+    def reset_carry(self):
+        _check("frsvt_reset_carry", lib.frsvt_reset_carry(self._h))
+
+    def set_call_index(self, call):
+        _check("frsvt_set_call_index", lib.frsvt_set_call_index(self._h, int(call)))
+
+    def info(self):
+        inf = FrsvtInfo()
+        _check("frsvt_get_info", lib.frsvt_get_info(self._h, ctypes.byref(inf)))
+        return inf
+
+    def get_mu(self):
+        v = ctypes.c_double(0.0)
+        _check("rpca_get_mu", lib.rpca_get_mu(self._h, ctypes.byref(v)))
+        return v.value
+
+    def set_mu(self, mu, mu_bar):
+        _check("rpca_set_mu", lib.rpca_set_mu(self._h, float(mu), float(mu_bar)))
+
+    def profile(self, enable=True):
+        _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{kind: (ms, launches, bytes)} for kinds 'AX', 'AtQ', 'compose'."""
+        out = {}
+        for k, name in enumerate(("AX", "AtQ", "compose")):
+            ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+            _check("frsvt_profile_read", lib.frsvt_profile_read(self._h, k, ctypes.byref(ms), ctypes.byref(n),
+                                                                ctypes.byref(b)))
+            out[name] = (ms.value, n.value, b.value)
+        return out
+
+    @property
+    def launches(self):
+        return int(lib.frsvt_kernel_launches(self._h))

@@ -1,0 +1,756 @@
+// libfrsvt: C ABI + orchestration of the FRSVT hot path on one B200 rank.
+// Declarations, argument meaning and error behaviour: include/frsvt.h.
+//
+// One call of frsvt_apply* / rpca_alm_step enqueues, on the handle's stream:
+//   omega -> Y = A Omega' (+ Q~)                          sketch   (Alg. 1 l.3-11)
+//   orth(Y) = CholeskyQR2 (fp64 Gram, pivoted Cholesky)     rank reveal
+//   q x { Z = orth(A^T Q); Y = A Z; Q = orth(Y) }           power iteration (l.13-15)
+//   B^T = A^T Q; G = B B^T (fp64); Jacobi -> U_B, sigma     small SVD (l.16-18)
+//   shrink -> Mc, Mp; Q~ = Q Mc; Wt = B^T Mp                Eq. (6) factors
+//   X = Q~ Wt^T  (or the fused iALM epilogue)               composition (l.19)
+// Row-sharded operands are reduced over ranks with NCCL where the contraction
+// runs over rows (Grams of m-row matrices, A^T Q, residual, init norms).
+#include "../../include/frsvt.h"
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "small.cuh"
+
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+using namespace frsvt;
+
+namespace {
+
+struct DevState {
+  int s, r, flags, sweeps, have_prev, pad0, pad1, pad2;
+  double mu[2];        // mu_k, mu_bar
+  double tau;
+  double scal[4];      // 1/J, ||D||_2
+  double dmax, dss;    // ||D||_inf, ||D||_F^2
+  double resid[2];     // ||D-L-E||_F^2, relative residual
+  double rep[2 * FRSVT_LMAX];
+};
+
+struct Status {
+  frsvt_status st = FRSVT_OK;
+};
+
+}  // namespace
+
+struct frsvt_handle {
+  frsvt_config cfg;
+  cudaStream_t st;
+  int dev_id;
+  int esz;  // element size
+  int l, q, rp;
+  int64_t m, n;
+  // workspaces (element type = dtype)
+  void *Om, *OmOv, *Y, *Q, *Qtmp, *Qt, *Z, *Zq, *Zt, *Wt;
+  void *T1, *Mc, *Mp;
+  double *wvec;
+  void* partq;       // split-K partials of A^T Q (dtype)
+  size_t partq_elems;
+  double* partd;     // Gram split-K partials (fp64)
+  size_t partd_elems;
+  double* redpart;   // per-block reduction partials
+  size_t redpart_elems;
+  double *G, *UB, *sigma, *dprev;
+  double* redtmp;    // small fold outputs
+  DevState* dev;
+  int64_t call;
+  int override_pending;
+  ncclComm_t comm;
+  int64_t launches;
+  double last_mu_host;
+  // pass profiling (frsvt_profile)
+  int prof_on;
+  std::vector<cudaEvent_t>* prof_ev;   // pool, pairs (start, end)
+  std::vector<int>* prof_kind;         // kind per used pair
+  size_t prof_used;
+  double prof_ms[3], prof_bytes[3];
+  int64_t prof_count[3];
+};
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess) {                                                       \
+      fprintf(stderr, "libfrsvt: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(e_), \
+              __FILE__, __LINE__);                                                 \
+      return FRSVT_ECUDA;                                                          \
+    }                                                                              \
+  } while (0)
+
+#define CKN(x)                                                                     \
+  do {                                                                             \
+    ncclResult_t r_ = (x);                                                         \
+    if (r_ != ncclSuccess) {                                                       \
+      fprintf(stderr, "libfrsvt: %s failed: %s\n", #x, ncclGetErrorString(r_));    \
+      return FRSVT_ENCCL;                                                          \
+    }                                                                              \
+  } while (0)
+
+#define TRY(x)                         \
+  do {                                 \
+    frsvt_status s_ = (x);             \
+    if (s_ != FRSVT_OK) return s_;     \
+  } while (0)
+
+namespace {
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+frsvt_status post_launch(frsvt_handle* h) {
+  h->launches++;
+  CK(cudaGetLastError());
+  return FRSVT_OK;
+}
+
+frsvt_status prof_flush(frsvt_handle* h) {
+  if (!h->prof_used) return FRSVT_OK;
+  CK(cudaEventSynchronize((*h->prof_ev)[2 * h->prof_used - 1]));
+  for (size_t i = 0; i < h->prof_used; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, (*h->prof_ev)[2 * i], (*h->prof_ev)[2 * i + 1]));
+    h->prof_ms[(*h->prof_kind)[i]] += ms;
+  }
+  h->prof_used = 0;
+  return FRSVT_OK;
+}
+
+// bracket one streaming pass with events (no-op unless profiling)
+frsvt_status prof_begin(frsvt_handle* h) {
+  if (!h->prof_on) return FRSVT_OK;
+  if (2 * (h->prof_used + 1) > h->prof_ev->size()) {
+    if (h->prof_ev->size() < 2 * 8192) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        h->prof_ev->push_back(e);
+      }
+      h->prof_kind->resize(h->prof_ev->size() / 2);
+    } else {
+      TRY(prof_flush(h));
+    }
+  }
+  CK(cudaEventRecord((*h->prof_ev)[2 * h->prof_used], h->st));
+  return FRSVT_OK;
+}
+frsvt_status prof_end(frsvt_handle* h, int kind, double bytes) {
+  if (!h->prof_on) return FRSVT_OK;
+  CK(cudaEventRecord((*h->prof_ev)[2 * h->prof_used + 1], h->st));
+  (*h->prof_kind)[h->prof_used] = kind;
+  h->prof_used++;
+  h->prof_bytes[kind] += bytes;
+  h->prof_count[kind]++;
+  return FRSVT_OK;
+}
+
+int grid1d(int64_t total, int threads = 256) {
+  int64_t b = cdiv(total, threads);
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------- GEMM glue
+template <typename Tin, typename Tacc, int BM, int BN, int BK, int TM, int TN, bool AMC, bool BKC,
+          class Epi>
+frsvt_status launch_tile(frsvt_handle* h, int M, int N, int K, int splits, const Tin* A,
+                         int64_t lda, const Tin* B, int64_t ldb, const int* kdev, Epi epi) {
+  if (M <= 0 || N <= 0) return FRSVT_OK;
+  if (splits < 1) splits = 1;
+  int kchunk = (int)cdiv(cdiv(K, splits), BK) * BK;
+  if (kchunk < BK) kchunk = BK;
+  dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)splits);
+  gemm_simt_kernel<Tin, Tacc, BM, BN, BK, TM, TN, AMC, BKC, Epi>
+      <<<grid, 256, 0, h->st>>>(M, N, K, kchunk, A, lda, B, ldb, kdev, epi);
+  return post_launch(h);
+}
+
+// skinny: N = l (<= 128)
+template <typename Tin, typename Tacc, bool AMC, bool BKC, class Epi>
+frsvt_status launch_skinny(frsvt_handle* h, int M, int N, int K, int splits, const Tin* A,
+                           int64_t lda, const Tin* B, int64_t ldb, const int* kdev, Epi epi) {
+  if (N <= 16)
+    return launch_tile<Tin, Tacc, 256, 16, 16, 4, 4, AMC, BKC>(h, M, N, K, splits, A, lda, B, ldb, kdev, epi);
+  if (N <= 32)
+    return launch_tile<Tin, Tacc, 128, 32, 16, 4, 4, AMC, BKC>(h, M, N, K, splits, A, lda, B, ldb, kdev, epi);
+  if (N <= 64)
+    return launch_tile<Tin, Tacc, 128, 64, 16, 8, 4, AMC, BKC>(h, M, N, K, splits, A, lda, B, ldb, kdev, epi);
+  return launch_tile<Tin, Tacc, 128, 128, 16, 8, 8, AMC, BKC>(h, M, N, K, splits, A, lda, B, ldb, kdev, epi);
+}
+
+// square l x l outputs (Gram)
+template <typename Tin, class Epi>
+frsvt_status launch_gram_tile(frsvt_handle* h, int l, int K, int splits, const Tin* Y, int64_t ld,
+                              Epi epi) {
+  if (l <= 16)
+    return launch_tile<Tin, double, 16, 16, 32, 1, 1, false, true>(h, l, l, K, splits, Y, ld, Y, ld, nullptr, epi);
+  if (l <= 32)
+    return launch_tile<Tin, double, 32, 32, 16, 2, 2, false, true>(h, l, l, K, splits, Y, ld, Y, ld, nullptr, epi);
+  if (l <= 64)
+    return launch_tile<Tin, double, 64, 64, 16, 4, 4, false, true>(h, l, l, K, splits, Y, ld, Y, ld, nullptr, epi);
+  return launch_tile<Tin, double, 128, 128, 16, 8, 8, false, true>(h, l, l, K, splits, Y, ld, Y, ld, nullptr, epi);
+}
+
+int gram_splits(int64_t rows) {
+  int64_t s = cdiv(rows, 256);
+  if (s > 296) s = 296;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+int atq_splits(int64_t n, int64_t rows, int l) {
+  const int bm = l <= 16 ? 256 : 128;
+  int64_t tiles = cdiv(n, bm);
+  int64_t s = cdiv(296, tiles);
+  int64_t maxs = cdiv(rows, 128);
+  if (s > maxs) s = maxs;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+frsvt_status allreduce(frsvt_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
+  if (h->cfg.nranks <= 1) return FRSVT_OK;
+  CKN(ncclAllReduce(buf, buf, count, t, op, h->comm, h->st));
+  return FRSVT_OK;
+}
+
+template <typename T> ncclDataType_t nccl_type();
+template <> ncclDataType_t nccl_type<float>() { return ncclFloat32; }
+template <> ncclDataType_t nccl_type<double>() { return ncclFloat64; }
+
+// G (l x l fp64) = Y^T Y over `rows` rows; summed over ranks if `sharded`.
+template <typename T>
+frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded) {
+  const int l = h->l;
+  const int S = gram_splits(rows);
+  EpiStore<double> epi{h->partd, l, (int64_t)l * l};
+  TRY(launch_gram_tile<T>(h, l, (int)rows, S, Y, ld, epi));
+  splitk_reduce_kernel<double, double><<<grid1d((int64_t)l * l), 256, 0, h->st>>>(h->partd, S, l, l, h->G, l);
+  TRY(post_launch(h));
+  if (sharded) TRY(allreduce(h, h->G, (size_t)l * l, ncclFloat64, ncclSum));
+  return FRSVT_OK;
+}
+
+template <typename T>
+frsvt_status chol(frsvt_handle* h, T* Tout) {
+  const int l = h->l;
+  const double tol = sizeof(T) == 4 ? 1e-12 : 1e-13;
+  const size_t smem = ((size_t)l * l + 3 * l) * sizeof(double) + 2 * l * sizeof(int);
+  chol_piv_kernel<T><<<1, 512, smem, h->st>>>(h->G, l, tol, Tout, &h->dev->s, &h->dev->flags);
+  return post_launch(h);
+}
+
+// Out (rows x l) = In (rows x l) * M (l x l)
+template <typename T>
+frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldin, const T* Msm,
+                         T* Out, int64_t ldout) {
+  EpiStore<T> epi{Out, ldout, 0};
+  return launch_skinny<T, T, true, true>(h, (int)rows, h->l, h->l, 1, In, ldin, Msm, (int64_t)h->l,
+                                          nullptr, epi);
+}
+
+// CholeskyQR2 with pivoted truncated Cholesky (reading R4/R5 in DESIGN.md)
+template <typename T>
+frsvt_status orth(frsvt_handle* h, const T* In, int64_t rows, T* Out, T* Tmp, bool sharded) {
+  TRY(gram<T>(h, In, rows, rows, sharded));
+  TRY(chol<T>(h, (T*)h->T1));
+  TRY(apply_small<T>(h, In, rows, rows, (const T*)h->T1, Tmp, rows));
+  TRY(gram<T>(h, Tmp, rows, rows, sharded));
+  TRY(chol<T>(h, (T*)h->T1));
+  TRY(apply_small<T>(h, Tmp, rows, rows, (const T*)h->T1, Out, rows));
+  return FRSVT_OK;
+}
+
+// Y (m x l) = A (m x n) * X (n x l)  [+ Add]
+template <typename T>
+frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y, const T* Add) {
+  TRY(prof_begin(h));
+  if (Add) {
+    EpiStoreAdd<T> epi{Y, h->m, Add, h->m};
+    TRY((launch_skinny<T, T, true, true>(h, (int)h->m, h->l, (int)h->n, 1, A, lda, X, h->n, nullptr, epi)));
+  } else {
+    EpiStore<T> epi{Y, h->m, 0};
+    TRY((launch_skinny<T, T, true, true>(h, (int)h->m, h->l, (int)h->n, 1, A, lda, X, h->n, nullptr, epi)));
+  }
+  return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
+}
+
+// Z (n x l) = A^T (n x m) * Q (m x l), split-K over rows, all-reduced over ranks
+template <typename T>
+frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z) {
+  const int S = atq_splits(h->n, h->m, h->l);
+  EpiStore<T> epi{(T*)h->partq, h->n, (int64_t)h->n * h->l};
+  TRY(prof_begin(h));
+  TRY((launch_skinny<T, T, false, true>(h, (int)h->n, h->l, (int)h->m, S, A, lda, Q, h->m, nullptr, epi)));
+  TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
+  splitk_reduce_kernel<T, T><<<grid1d(h->n * h->l), 256, 0, h->st>>>((const T*)h->partq, S, (int)h->n, h->l, Z, h->n);
+  TRY(post_launch(h));
+  TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
+  return FRSVT_OK;
+}
+
+// range finder: Q (m x l) spanning (A A^T)^q A Omega' (+ Q~), Alg. 1 lines 3-15
+template <typename T>
+frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint32_t stream,
+                          bool use_carry, int64_t call) {
+  const int l = h->l;
+  const T* ov = h->override_pending ? (const T*)h->OmOv : nullptr;
+  omega_kernel<T><<<grid1d(h->n * l), 256, 0, h->st>>>((T*)h->Om, h->n, l, &h->dev->r, use_carry ? 1 : 0,
+                                                       h->cfg.seed, stream + (uint32_t)call, ov, h->n);
+  TRY(post_launch(h));
+  h->override_pending = 0;
+  TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
+  const bool sh = h->cfg.nranks > 1;
+  TRY(orth<T>(h, (const T*)h->Y, h->m, (T*)h->Q, (T*)h->Qtmp, sh));
+  for (int it = 0; it < q; ++it) {
+    TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
+    TRY(orth<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, (T*)h->Zt, false));
+    TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr));
+    TRY(orth<T>(h, (const T*)h->Y, h->m, (T*)h->Q, (T*)h->Qtmp, sh));
+  }
+  return FRSVT_OK;
+}
+
+// B^T = A^T Q, G = B B^T, Jacobi -> sigma, U_B   (Alg. 1 lines 16-18)
+template <typename T>
+frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda) {
+  const int l = h->l;
+  TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
+  TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
+  const size_t smem = ((size_t)l * (l + 1) / 2 + (size_t)l * l + FRSVT_LMAX) * sizeof(double) +
+                      3 * (FRSVT_LMAX / 2) * sizeof(int);
+  jacobi_eig_kernel<<<1, 1024, smem, h->st>>>(h->G, l, 40, h->sigma, h->UB, &h->dev->sweeps,
+                                               &h->dev->flags);
+  return post_launch(h);
+}
+
+// shrink + factors: Q~ = Q Mc, Wt = B^T Mp (Eq. 6 with the kept set)
+template <typename T>
+frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const double* tau_dev,
+                                double C, double eps) {
+  const int l = h->l;
+  shrink_kernel<T><<<1, 128, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec,
+                                         C, eps, h->dprev, &h->dev->have_prev, (T*)h->Mc, (T*)h->Mp,
+                                         &h->dev->r, &h->dev->flags, h->dev->rep);
+  TRY(post_launch(h));
+  TRY(apply_small<T>(h, (const T*)h->Q, h->m, h->m, (const T*)h->Mc, (T*)h->Qt, h->m));
+  TRY(apply_small<T>(h, (const T*)h->Z, h->n, h->n, (const T*)h->Mp, (T*)h->Wt, h->n));
+  return FRSVT_OK;
+}
+
+template <typename T>
+frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, double tau,
+                        const double* tau_dev, double C, double eps) {
+  TRY(range_finder<T>(h, A, lda, h->q, 1000u, h->rp != 0, h->call));
+  TRY(small_svd<T>(h, A, lda));
+  TRY(shrink_and_factors<T>(h, wmode, tau, tau_dev, C, eps));
+  h->call++;
+  return FRSVT_OK;
+}
+
+// X = Q~ Wt^T  (reconstruction, K = r)
+template <typename T>
+frsvt_status compose_X(frsvt_handle* h, T* X, int64_t ldx) {
+  EpiStore<T> epi{X, ldx, 0};
+  TRY(prof_begin(h));
+  TRY((launch_tile<T, T, 128, 128, 16, 8, 8, true, false>(h, (int)h->m, (int)h->n, h->l, 1,
+                                                         (const T*)h->Qt, h->m, (const T*)h->Wt,
+                                                         h->n, &h->dev->r, epi)));
+  return prof_end(h, 2, (double)h->m * h->n * sizeof(T));
+}
+
+frsvt_status fill_info(frsvt_handle* h, frsvt_info* info) {
+  if (!info) return FRSVT_OK;
+  CK(cudaStreamSynchronize(h->st));
+  DevState ds;
+  CK(cudaMemcpy(&ds, h->dev, sizeof(DevState), cudaMemcpyDeviceToHost));
+  memset(info, 0, sizeof(*info));
+  info->s = ds.s;
+  info->r = ds.r;
+  info->flags = ds.flags;
+  info->sweeps = ds.sweeps;
+  info->calls = h->call;
+  info->mu = ds.mu[0];
+  for (int i = 0; i < FRSVT_LMAX; ++i) {
+    info->sigma[i] = i < h->l ? ds.rep[i] : 0.0;
+    info->d[i] = i < h->l ? ds.rep[FRSVT_LMAX + i] : 0.0;
+  }
+  if (ds.flags & FLAG_NONFINITE) return FRSVT_ENONFINITE;
+  return FRSVT_OK;
+}
+
+template <typename T>
+frsvt_status apply_impl(frsvt_handle* h, const void* A, int64_t lda, int wmode, double tau,
+                        const double* w_host, double C, double eps, void* X, int64_t ldx,
+                        frsvt_info* info) {
+  if (wmode == 1) CK(cudaMemcpyAsync(h->wvec, w_host, sizeof(double) * h->l, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  TRY(frsvt_core<T>(h, (const T*)A, lda, wmode, tau, nullptr, C, eps));
+  TRY(compose_X<T>(h, (T*)X, ldx));
+  return fill_info(h, info);
+}
+
+// ||D||_2 estimate: block power (Rayleigh-Ritz on l columns), used only when
+// the caller does not supply ||D||_2 (reading Z10). Writes sigma[0].
+template <typename T>
+frsvt_status estimate_norm2(frsvt_handle* h, const T* D, int64_t ld) {
+  CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
+  TRY(range_finder<T>(h, D, ld, 6, 999u, false, 0));
+  TRY(small_svd<T>(h, D, ld));
+  return FRSVT_OK;
+}
+
+template <typename T>
+frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* rel_resid) {
+  const double lambda = st->lambda > 0 ? st->lambda : 1.0 / sqrt((double)(h->cfg.m_global > h->n ? h->cfg.m_global : h->n));
+  const T* D = (const T*)st->D;
+  T* E = (T*)st->E;
+  T* A = (T*)st->A;
+  CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  if (st->iter == 0) {
+    // ---- init: norms, mu_0, Y_0, E_1, A_1 ----
+    const int nb = grid1d(h->m * h->n);
+    absmax_sumsq_kernel<T><<<nb, 256, 0, h->st>>>(D, h->m, h->n, st->ld, h->redpart, h->redpart + nb);
+    TRY(post_launch(h));
+    fold_kernel<<<1, 256, 0, h->st>>>(h->redpart, h->redpart + nb, nb, &h->dev->dmax, &h->dev->dss);
+    TRY(post_launch(h));
+    TRY(allreduce(h, &h->dev->dmax, 1, ncclFloat64, ncclMax));
+    TRY(allreduce(h, &h->dev->dss, 1, ncclFloat64, ncclSum));
+    if (!(st->norm2_D > 0)) TRY(estimate_norm2<T>(h, D, st->ld));
+    alm_scalars_kernel<<<1, 1, 0, h->st>>>(st->norm2_D, h->sigma, st->mu0, st->mu_max_factor, lambda,
+                                           &h->dev->dmax, h->dev->mu, h->dev->scal);
+    TRY(post_launch(h));
+    alm_init_kernel<T><<<nb, 256, 0, h->st>>>(D, E, A, h->m, h->n, st->ld, h->dev->mu, h->dev->scal, lambda);
+    TRY(post_launch(h));
+    // fresh solve: empty carry, Omega sequence restarts at call 0
+    CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
+    CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
+    CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
+    h->call = 0;
+  }
+  tau_from_mu_kernel<<<1, 1, 0, h->st>>>(h->dev->mu, &h->dev->tau);
+  TRY(post_launch(h));
+  TRY(frsvt_core<T>(h, A, st->ld, 0, 0.0, &h->dev->tau, 0.0, 0.0));
+  // fused reconstruction + iALM epilogue (one pass over D, A, E)
+  const int gx = (int)cdiv(h->m, 128), gy = (int)cdiv(h->n, 128);
+  EpiAlm<T> epi{D, A, E, (T*)st->L, st->ld, h->dev->mu, st->rho, lambda, finalize, h->redpart};
+  TRY(prof_begin(h));
+  TRY((launch_tile<T, T, 128, 128, 16, 8, 8, true, false>(h, (int)h->m, (int)h->n, h->l, 1,
+                                                         (const T*)h->Qt, h->m, (const T*)h->Wt, h->n,
+                                                         &h->dev->r, epi)));
+  TRY(prof_end(h, 2, (double)h->m * h->n * sizeof(T) * (finalize ? 3.0 : 5.0)));
+  fold_sum_kernel<<<1, 256, 0, h->st>>>(h->redpart, gx * gy, &h->dev->resid[0]);
+  TRY(post_launch(h));
+  TRY(allreduce(h, &h->dev->resid[0], 1, ncclFloat64, ncclSum));
+  alm_mu_kernel<<<1, 1, 0, h->st>>>(st->rho, finalize, h->dev->mu, &h->dev->dss, h->dev->resid);
+  TRY(post_launch(h));
+  if (!finalize) st->iter++;
+  if (rel_resid) {
+    CK(cudaStreamSynchronize(h->st));
+    CK(cudaMemcpy(rel_resid, &h->dev->resid[1], sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return FRSVT_OK;
+}
+
+template <typename T>
+void set_smem_attrs() {
+  const int l = FRSVT_LMAX;
+  const size_t chol_smem = ((size_t)l * l + 3 * l) * sizeof(double) + 2 * l * sizeof(int);
+  cudaFuncSetAttribute(chol_piv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+const char* frsvt_status_string(frsvt_status s) {
+  switch (s) {
+    case FRSVT_OK: return "ok";
+    case FRSVT_EINVAL: return "invalid argument";
+    case FRSVT_ENOCONV: return "Jacobi sweep cap reached";
+    case FRSVT_ECUDA: return "CUDA error";
+    case FRSVT_ENCCL: return "NCCL error";
+    case FRSVT_ENONFINITE: return "non-finite value reached a Gram diagonal";
+    case FRSVT_ENOMEM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
+  if (!out) return FRSVT_EINVAL;
+  ncclUniqueId id;
+  CKN(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(out, &id, 128);
+  return FRSVT_OK;
+}
+
+static void free_handle(frsvt_handle* h) {
+  if (!h) return;
+  void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
+                  h->Mp, h->wvec, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
+                  h->redtmp, h->dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->prof_ev) {
+    for (cudaEvent_t e : *h->prof_ev) cudaEventDestroy(e);
+    delete h->prof_ev;
+  }
+  delete h->prof_kind;
+  delete h;
+}
+
+frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_handle** out) {
+  if (!out) return FRSVT_EINVAL;
+  *out = nullptr;
+  if (!cfg) return FRSVT_EINVAL;
+  const frsvt_config& c = *cfg;
+  if (c.dtype != FRSVT_F32 && c.dtype != FRSVT_F64) return FRSVT_EINVAL;
+  if (c.m_local < 1 || c.n < 1 || c.m_global < c.m_local || c.row0 < 0 || c.row0 + c.m_local > c.m_global)
+    return FRSVT_EINVAL;
+  if (c.l < 1 || c.l > FRSVT_LMAX || c.l > c.n || c.l > c.m_global || c.l > c.m_local) return FRSVT_EINVAL;
+  if (c.q < 0 || c.q > 64) return FRSVT_EINVAL;
+  if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) return FRSVT_EINVAL;
+  if (c.nranks == 1 && c.m_local != c.m_global) return FRSVT_EINVAL;
+  if (c.nranks > 1 && !c.nccl_id) return FRSVT_EINVAL;
+  if (c.m_local > (int64_t)INT32_MAX || c.n > (int64_t)INT32_MAX) return FRSVT_EINVAL;
+
+  frsvt_handle* h = new (std::nothrow) frsvt_handle();
+  if (!h) return FRSVT_ENOMEM;
+  memset(h, 0, sizeof(*h));
+  h->cfg = c;
+  h->cfg.nccl_id = nullptr;
+  h->st = (cudaStream_t)cuda_stream;
+  cudaGetDevice(&h->dev_id);
+  h->esz = c.dtype == FRSVT_F32 ? 4 : 8;
+  h->l = c.l;
+  h->q = c.q;
+  h->rp = c.range_propagation ? 1 : 0;
+  h->m = c.m_local;
+  h->n = c.n;
+  h->prof_ev = new (std::nothrow) std::vector<cudaEvent_t>();
+  h->prof_kind = new (std::nothrow) std::vector<int>();
+  if (!h->prof_ev || !h->prof_kind) {
+    free_handle(h);
+    return FRSVT_ENOMEM;
+  }
+  const int l = c.l;
+  const size_t ml = (size_t)h->m * l * h->esz, nl = (size_t)h->n * l * h->esz, ll = (size_t)l * l * h->esz;
+  const int S_atq = atq_splits(h->n, h->m, l);
+  h->partq_elems = (size_t)S_atq * h->n * l;
+  const int64_t maxrows = h->m > h->n ? h->m : h->n;
+  h->partd_elems = (size_t)gram_splits(maxrows) * l * l;
+  const int64_t gx = cdiv(h->m, 128), gy = cdiv(h->n, 128);
+  h->redpart_elems = (size_t)(gx * gy > 2 * 148 * 16 ? gx * gy : 2 * 148 * 16) + 64;
+  struct {
+    void** p;
+    size_t bytes;
+  } allocs[] = {{&h->Om, nl},          {&h->OmOv, nl},         {&h->Y, ml},
+                {&h->Q, ml},           {&h->Qtmp, ml},         {&h->Qt, ml},
+                {&h->Z, nl},           {&h->Zq, nl},           {&h->Zt, nl},
+                {&h->Wt, nl},          {&h->T1, ll},           {&h->Mc, ll},
+                {&h->Mp, ll},          {(void**)&h->wvec, sizeof(double) * FRSVT_LMAX},
+                {&h->partq, h->partq_elems * h->esz},
+                {(void**)&h->partd, h->partd_elems * sizeof(double)},
+                {(void**)&h->redpart, h->redpart_elems * sizeof(double)},
+                {(void**)&h->G, sizeof(double) * l * l},
+                {(void**)&h->UB, sizeof(double) * l * l},
+                {(void**)&h->sigma, sizeof(double) * FRSVT_LMAX},
+                {(void**)&h->dprev, sizeof(double) * FRSVT_LMAX},
+                {(void**)&h->redtmp, sizeof(double) * 64},
+                {(void**)&h->dev, sizeof(DevState)}};
+  for (auto& a : allocs) {
+    if (cudaMalloc(a.p, a.bytes) != cudaSuccess) {
+      cudaGetLastError();
+      free_handle(h);
+      return FRSVT_ENOMEM;
+    }
+  }
+  cudaMemset(h->Qt, 0, ml);
+  cudaMemset(h->dev, 0, sizeof(DevState));
+  cudaMemset(h->sigma, 0, sizeof(double) * FRSVT_LMAX);
+  cudaMemset(h->dprev, 0, sizeof(double) * FRSVT_LMAX);
+  set_smem_attrs<float>();
+  set_smem_attrs<double>();
+  {
+    const size_t jsmem = ((size_t)FRSVT_LMAX * (FRSVT_LMAX + 1) / 2 + (size_t)FRSVT_LMAX * FRSVT_LMAX +
+                          FRSVT_LMAX) * sizeof(double) + 3 * (FRSVT_LMAX / 2) * sizeof(int);
+    cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsmem);
+  }
+  if (c.nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, c.nccl_id, 128);
+    if (ncclCommInitRank(&h->comm, c.nranks, id, c.rank) != ncclSuccess) {
+      free_handle(h);
+      return FRSVT_ENCCL;
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    free_handle(h);
+    return FRSVT_ECUDA;
+  }
+  *out = h;
+  return FRSVT_OK;
+}
+
+void frsvt_destroy(frsvt_handle* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->st);
+  free_handle(h);
+}
+
+frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau, void* X, int64_t ldx,
+                         frsvt_info* info) {
+  if (!h || !A || !X || lda < h->m || ldx < h->m || !(tau >= 0) || !std::isfinite(tau)) return FRSVT_EINVAL;
+  if (h->cfg.dtype == FRSVT_F32) return apply_impl<float>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
+  return apply_impl<double>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
+}
+
+frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda, int32_t wmode,
+                                  const double* w, double C, double eps, void* X, int64_t ldx,
+                                  frsvt_info* info) {
+  if (!h || !A || !X || lda < h->m || ldx < h->m) return FRSVT_EINVAL;
+  int km;
+  if (wmode == 0) {
+    if (!w) return FRSVT_EINVAL;
+    for (int i = 0; i < h->l; ++i)
+      if (!(w[i] >= 0) || !std::isfinite(w[i])) return FRSVT_EINVAL;
+    km = 1;
+  } else if (wmode == 1 || wmode == 2) {
+    if (!(C >= 0) || !std::isfinite(C) || !(eps > 0) || !std::isfinite(eps)) return FRSVT_EINVAL;
+    km = wmode == 1 ? 2 : 3;
+  } else {
+    return FRSVT_EINVAL;
+  }
+  if (h->cfg.dtype == FRSVT_F32) return apply_impl<float>(h, A, lda, km, 0.0, w, C, eps, X, ldx, info);
+  return apply_impl<double>(h, A, lda, km, 0.0, w, C, eps, X, ldx, info);
+}
+
+frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, double* rel_resid) {
+  if (!h || !st || !st->D || !st->E || !st->A || st->ld < h->m) return FRSVT_EINVAL;
+  if (finalize && !st->L) return FRSVT_EINVAL;
+  if (!(st->rho > 1.0) || !std::isfinite(st->rho)) return FRSVT_EINVAL;
+  if (st->iter < 0) return FRSVT_EINVAL;
+  if (st->iter == 0 && !(st->mu_max_factor >= 1.0)) return FRSVT_EINVAL;
+  if (st->norm2_D < 0 || st->mu0 < 0 || !std::isfinite(st->norm2_D) || !std::isfinite(st->mu0)) return FRSVT_EINVAL;
+  if (h->cfg.dtype == FRSVT_F32) return rpca_impl<float>(h, st, finalize, rel_resid);
+  return rpca_impl<double>(h, st, finalize, rel_resid);
+}
+
+frsvt_status frsvt_set_omega(frsvt_handle* h, const void* Om, int64_t ldo) {
+  if (!h || !Om || ldo < h->n) return FRSVT_EINVAL;
+  CK(cudaMemcpy2DAsync(h->OmOv, h->n * h->esz, Om, ldo * h->esz, h->n * h->esz, h->l,
+                       cudaMemcpyDeviceToDevice, h->st));
+  h->override_pending = 1;
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_draw_omega(frsvt_handle* h, int64_t call, void* out, int64_t ldo) {
+  if (!h || !out || ldo < h->n || call < 0) return FRSVT_EINVAL;
+  if (h->cfg.dtype == FRSVT_F32)
+    omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 0,
+                                                               h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n);
+  else
+    omega_kernel<double><<<grid1d(h->n * h->l), 256, 0, h->st>>>((double*)h->Om, h->n, h->l, &h->dev->r, 0,
+                                                                h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n);
+  TRY(post_launch(h));
+  CK(cudaMemcpy2DAsync(out, ldo * h->esz, h->Om, h->n * h->esz, h->n * h->esz, h->l, cudaMemcpyDeviceToDevice,
+                       h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_get_carry(frsvt_handle* h, void* Qt, int64_t ldq, int32_t* r) {
+  if (!h || !Qt || ldq < h->m) return FRSVT_EINVAL;
+  CK(cudaMemcpy2DAsync(Qt, ldq * h->esz, h->Qt, h->m * h->esz, h->m * h->esz, h->l, cudaMemcpyDeviceToDevice,
+                       h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (r) {
+    int rr = 0;
+    CK(cudaMemcpy(&rr, &h->dev->r, sizeof(int), cudaMemcpyDeviceToHost));
+    *r = rr;
+  }
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_set_carry(frsvt_handle* h, const void* Qt, int64_t ldq, int32_t r) {
+  if (!h || r < 0 || r > h->l || (r > 0 && (!Qt || ldq < h->m))) return FRSVT_EINVAL;
+  CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
+  if (r > 0)
+    CK(cudaMemcpy2DAsync(h->Qt, h->m * h->esz, Qt, ldq * h->esz, h->m * h->esz, r, cudaMemcpyDeviceToDevice,
+                         h->st));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(&h->dev->r, &r, sizeof(int), cudaMemcpyHostToDevice));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_reset_carry(frsvt_handle* h) {
+  if (!h) return FRSVT_EINVAL;
+  CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
+  CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
+  CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_set_call_index(frsvt_handle* h, int64_t call) {
+  if (!h || call < 0) return FRSVT_EINVAL;
+  h->call = call;
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_get_info(frsvt_handle* h, frsvt_info* info) {
+  if (!h || !info) return FRSVT_EINVAL;
+  return fill_info(h, info);
+}
+
+frsvt_status rpca_get_mu(frsvt_handle* h, double* mu) {
+  if (!h || !mu) return FRSVT_EINVAL;
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(mu, h->dev->mu, sizeof(double), cudaMemcpyDeviceToHost));
+  return FRSVT_OK;
+}
+
+frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar) {
+  if (!h || !(mu > 0) || !(mu_bar >= mu)) return FRSVT_EINVAL;
+  double v[2] = {mu, mu_bar};
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(h->dev->mu, v, sizeof(v), cudaMemcpyHostToDevice));
+  return FRSVT_OK;
+}
+
+int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : -1; }
+
+frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable) {
+  if (!h) return FRSVT_EINVAL;
+  CK(cudaStreamSynchronize(h->st));
+  h->prof_used = 0;
+  for (int k = 0; k < 3; ++k) {
+    h->prof_ms[k] = 0.0;
+    h->prof_bytes[k] = 0.0;
+    h->prof_count[k] = 0;
+  }
+  h->prof_on = enable ? 1 : 0;
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_profile_read(frsvt_handle* h, int32_t kind, double* ms, int64_t* launches, double* bytes) {
+  if (!h || kind < 0 || kind > 2) return FRSVT_EINVAL;
+  TRY(prof_flush(h));
+  if (ms) *ms = h->prof_ms[kind];
+  if (launches) *launches = h->prof_count[kind];
+  if (bytes) *bytes = h->prof_bytes[kind];
+  return FRSVT_OK;
+}
+
+}  // extern "C"

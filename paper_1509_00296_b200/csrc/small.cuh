@@ -1,0 +1,490 @@
+// Small-matrix and elementwise kernels of libfrsvt (sm_100a).
+//   omega_kernel     : Gaussian test matrix Omega
+//   chol_piv_kernel  : pivoted, truncated Cholesky of an equilibrated fp64
+//                      Gram (CholeskyQR rank reveal, the QR-CP of P:163/P:177)
+//   jacobi_eig_kernel: cyclic two-sided Jacobi on the l x l fp64 Gram B B^T
+//                      -> U_B, sigma (the small SVD of B, Eq. 6)
+//   shrink_kernel    : thresholds t_i, d_i = max(sigma_i - t_i, 0), kept set,
+//                      the l x l factors of Eq. (6)
+//   reductions, ALM init, split-K reduce.
+#pragma once
+#include "common.cuh"
+
+namespace frsvt {
+
+// ---- Philox4x32-10 + Box-Muller (same stream layout as synth/philox.py) ----
+__device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                         uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+}
+__device__ __forceinline__ double u53(uint32_t x0, uint32_t x1) {
+  return ((double)(x0 >> 5) * 67108864.0 + (double)(x1 >> 6)) * (1.0 / 9007199254740992.0);
+}
+__device__ __forceinline__ double philox_normal(uint64_t seed, uint32_t stream, uint64_t e) {
+  const uint64_t t = e >> 1;
+  uint32_t c0 = (uint32_t)t, c1 = (uint32_t)(t >> 32), c2 = stream, c3 = 0u;
+  philox10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const double ua = u53(c0, c1), ub = u53(c2, c3);
+  const double rad = sqrt(-2.0 * log1p(-ua));
+  const double ang = 6.283185307179586 * ub;
+  return (e & 1) ? rad * sin(ang) : rad * cos(ang);
+}
+
+// Omega' (n x l, ld n): columns [r, r+p) hold columns [0, p) of Omega of this
+// call (p = l - r, RP reading Z6), columns < r are zero so that
+// A * Omega' + Q~ = [Q~ | A Omega_p]. r = 0 without a carry.
+template <typename T>
+__global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __restrict__ r_dev,
+                             int use_r, uint64_t seed, uint32_t stream,
+                             const T* __restrict__ override_om, int64_t ldo) {
+  const int r = use_r ? *r_dev : 0;
+  const int64_t total = n * (int64_t)l;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % n;
+    const int c = (int)(idx / n);
+    T v = T(0);
+    if (c >= r) {
+      const int src = c - r;
+      if (override_om) v = override_om[i + src * ldo];
+      else v = (T)philox_normal(seed, stream, (uint64_t)src * (uint64_t)n + (uint64_t)i);
+    }
+    Om[idx] = v;
+  }
+}
+
+// ---- split-K reduction (fixed order => deterministic) ----------------------
+template <typename Tp, typename Tout>
+__global__ void splitk_reduce_kernel(const Tp* __restrict__ part, int S, int M, int N,
+                                     Tout* __restrict__ C, int64_t ldc) {
+  const int64_t MN = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < MN;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    Tp s = Tp(0);
+    for (int z = 0; z < S; ++z) s += part[z * MN + idx];
+    const int i = (int)(idx % M), j = (int)(idx / M);
+    C[i + (int64_t)j * ldc] = (Tout)s;
+  }
+}
+
+// ---- pivoted truncated Cholesky (single CTA, fp64, matrix in shared mem) ---
+// Input : G (l x l fp64 Gram, column-major, ld l).
+// Output: T (l x l, ld l) with Y*T = orth(Y) restricted to the revealed rank s:
+//         T[piv_k, j] = dsc[piv_k] * Rinv[k][j] for k <= j < s, 0 elsewhere,
+//         where diag(dsc) G diag(dsc) (unit diagonal) = Pi R^T R Pi^T.
+// A column whose equilibrated Schur diagonal falls to <= tol is numerically
+// dependent and truncates the factorisation (s = #pivots accepted).
+template <typename Tout>
+__global__ void __launch_bounds__(512)
+chol_piv_kernel(const double* __restrict__ G, int l, double tol, Tout* __restrict__ T,
+                int* __restrict__ s_out, int* __restrict__ flags) {
+  extern __shared__ double sm[];
+  double* S = sm;              // l*l, row-major
+  double* dsc = S + l * l;     // l
+  double* xt = dsc + l;        // l
+  double* dinv = xt + l;       // l
+  int* piv = (int*)(dinv + l); // l
+  int* ipiv = piv + l;         // l
+  __shared__ int s_sh, js_sh;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+
+  for (int i = tid; i < l; i += nt) {
+    const double g = G[i + (int64_t)i * l];
+    if (!isfinite(g)) atomicOr(flags, FLAG_NONFINITE);
+    dsc[i] = (g > 0.0 && isfinite(g)) ? 1.0 / sqrt(g) : 0.0;
+    piv[i] = i;
+  }
+  if (tid == 0) s_sh = l;
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int i = idx / l, c = idx % l;
+    double v = G[i + (int64_t)c * l] * dsc[i] * dsc[c];
+    S[idx] = isfinite(v) ? v : 0.0;
+  }
+  __syncthreads();
+
+  for (int k = 0; k < l; ++k) {
+    if (warp == 0) {
+      double best = -1.0;
+      int bj = l;
+      for (int j = k + lane; j < l; j += 32) {
+        const double v = S[j * l + j];
+        if (v > best) { best = v; bj = j; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+      }
+      if (lane == 0) {
+        js_sh = bj;
+        if (!(best > tol)) s_sh = k;
+      }
+    }
+    __syncthreads();
+    if (s_sh == k) break;
+    const int js = js_sh;
+    if (js != k) {
+      for (int i = tid; i < l; i += nt) {
+        const double a = S[i * l + k];
+        S[i * l + k] = S[i * l + js];
+        S[i * l + js] = a;
+      }
+      __syncthreads();
+      for (int c = tid; c < l; c += nt) {
+        const double a = S[k * l + c];
+        S[k * l + c] = S[js * l + c];
+        S[js * l + c] = a;
+      }
+      if (tid == 0) { const int p = piv[k]; piv[k] = piv[js]; piv[js] = p; }
+      __syncthreads();
+    }
+    const double rkk = sqrt(S[k * l + k]);
+    for (int c = k + 1 + tid; c < l; c += nt) S[k * l + c] /= rkk;
+    __syncthreads();
+    if (tid == 0) S[k * l + k] = rkk;
+    const int w = l - k - 1;
+    for (int idx = tid; idx < w * w; idx += nt) {
+      const int i = k + 1 + idx / w, c = k + 1 + idx % w;
+      S[i * l + c] -= S[k * l + i] * S[k * l + c];
+    }
+    __syncthreads();
+  }
+  const int s = s_sh;
+  // In-place inverse of the s x s upper triangle R (column sweep, dtrti2 order):
+  // Rinv[i][j] = -dinv[j] * (dinv[i] R[i][j] + sum_{i<k<j} Rinv[i][k] R[k][j]).
+  for (int j = tid; j < s; j += nt) dinv[j] = 1.0 / S[j * l + j];
+  __syncthreads();
+  for (int j = 1; j < s; ++j) {
+    for (int i = warp; i < j; i += nw) {
+      double acc = 0.0;
+      for (int kk = i + 1 + lane; kk < j; kk += 32) acc += S[i * l + kk] * S[kk * l + j];
+      acc = warp_sum(acc);
+      if (lane == 0) xt[i] = acc + dinv[i] * S[i * l + j];
+    }
+    __syncthreads();
+    for (int i = tid; i < j; i += nt) S[i * l + j] = -dinv[j] * xt[i];
+    __syncthreads();
+  }
+  for (int j = tid; j < s; j += nt) S[j * l + j] = dinv[j];
+  for (int k = tid; k < l; k += nt) ipiv[piv[k]] = k;
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int o = idx % l, j = idx / l;  // T[o + j*l]
+    const int k = ipiv[o];
+    double v = 0.0;
+    if (j < s && k <= j) v = dsc[o] * S[k * l + j];
+    T[idx] = (Tout)v;
+  }
+  if (tid == 0) *s_out = s;
+}
+
+// ---- cyclic two-sided Jacobi on the symmetric l x l fp64 Gram -------------
+// Packed upper storage of G, round-robin (circle) pair ordering so the l/2
+// rotations of a round are disjoint and applied in parallel as 2x2 blocks
+// J_a^T G_ab J_b; V accumulates V J. A pair rotates when
+// |g_pq| > max(1e-15 sqrt(g_pp g_qq), 4 eps g_max); a sweep with no rotation
+// ends the solve. Outputs sigma = sqrt(max(lambda, 0)) descending and the
+// matching columns of V (U_B, ld l) in fp64.
+__device__ __forceinline__ int pk_idx(int i, int j, int l) {
+  // packed upper index of (min, max)
+  const int a = i < j ? i : j, b = i < j ? j : i;
+  return a * l - (a * (a - 1)) / 2 + (b - a);
+}
+
+__global__ void __launch_bounds__(1024)
+jacobi_eig_kernel(const double* __restrict__ G, int l, int max_sweeps,
+                  double* __restrict__ sigma, double* __restrict__ UB,
+                  int* __restrict__ sweeps_out, int* __restrict__ flags) {
+  extern __shared__ double sm[];
+  const int np = l * (l + 1) / 2;
+  double* P = sm;                 // packed G
+  double* V = P + np;             // l*l column-major V[i + c*l]
+  double* cs = V + l * l;         // FRSVT_LMAX/2 * 2 (c, s) per pair
+  int* pp = (int*)(cs + FRSVT_LMAX);       // p of pair
+  int* qq = pp + FRSVT_LMAX / 2;           // q of pair
+  int* act = qq + FRSVT_LMAX / 2;          // active flag per pair
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int L2 = (l + 1) & ~1;  // even number of players (dummy = l if l odd)
+  const int h = L2 / 2;
+
+  double gmax_local = 0.0;
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int i = idx % l, c = idx / l;
+    const double g = G[idx];
+    if (i <= c) P[pk_idx(i, c, l)] = g;
+    V[idx] = (i == c) ? 1.0 : 0.0;
+    if (i == c) gmax_local = fmax(gmax_local, fabs(g));
+  }
+  const double gmax = block_max(gmax_local, red);
+  __shared__ double gmax_sh;
+  if (tid == 0) gmax_sh = gmax;
+  __syncthreads();
+  const double abs_thr = 4.0 * 2.220446049250313e-16 * gmax_sh;
+
+  int sweep = 0;
+  bool converged = false;
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int rnd = 0; rnd < L2 - 1; ++rnd) {
+      int a_loc = 0;
+      if (tid < h) {
+        // circle method: position 0 fixed, the others rotate by one per round
+        const int pos_a = tid, pos_b = L2 - 1 - tid;
+        int p = pos_a == 0 ? 0 : 1 + ((pos_a - 1 + rnd) % (L2 - 1));
+        int q = pos_b == 0 ? 0 : 1 + ((pos_b - 1 + rnd) % (L2 - 1));
+        if (p > q) { const int t = p; p = q; q = t; }
+        pp[tid] = p;
+        qq[tid] = q;
+        double c = 1.0, s = 0.0;
+        if (q < l) {
+          const double apq = P[pk_idx(p, q, l)];
+          const double app = P[pk_idx(p, p, l)];
+          const double aqq = P[pk_idx(q, q, l)];
+          const double thr = fmax(1e-15 * sqrt(fabs(app * aqq)), abs_thr);
+          if (fabs(apq) > thr) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            a_loc = 1;
+          }
+        }
+        cs[2 * tid] = c;
+        cs[2 * tid + 1] = s;
+        act[tid] = a_loc;
+      }
+      if (!__syncthreads_or(a_loc)) continue;
+      rotated = 1;
+      // G <- J^T G J, block (a, b) with b <= a
+      const int nblk = h * (h + 1) / 2;
+      for (int idx = tid; idx < nblk; idx += nt) {
+        int a = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+        while ((a + 1) * (a + 2) / 2 <= idx) ++a;
+        while (a * (a + 1) / 2 > idx) --a;
+        const int b = idx - a * (a + 1) / 2;
+        if (!act[a] && !act[b]) continue;
+        const int pa = pp[a], qa = qq[a], pb = pp[b], qb = qq[b];
+        const double ca = cs[2 * a], sa = cs[2 * a + 1];
+        const double cb = cs[2 * b], sb = cs[2 * b + 1];
+        if (a == b) {
+          const double app = P[pk_idx(pa, pa, l)], aqq = P[pk_idx(qa, qa, l)], apq = P[pk_idx(pa, qa, l)];
+          // J^T [[app,apq],[apq,aqq]] J with J = [[c, s], [-s, c]] (GVL symSchur2)
+          const double c2 = ca * ca, s2 = sa * sa, csx = ca * sa;
+          P[pk_idx(pa, pa, l)] = c2 * app - 2.0 * csx * apq + s2 * aqq;
+          P[pk_idx(qa, qa, l)] = s2 * app + 2.0 * csx * apq + c2 * aqq;
+          P[pk_idx(pa, qa, l)] = 0.0;
+        } else {
+          // rows {pa, qa} x cols {pb, qb}; the dummy player (index l) is absent
+          const bool ra = qa < l, rb = qb < l;
+          const double m00 = P[pk_idx(pa, pb, l)];
+          const double m01 = rb ? P[pk_idx(pa, qb, l)] : 0.0;
+          const double m10 = ra ? P[pk_idx(qa, pb, l)] : 0.0;
+          const double m11 = (ra && rb) ? P[pk_idx(qa, qb, l)] : 0.0;
+          const double n00 = ca * m00 - sa * m10, n01 = ca * m01 - sa * m11;
+          const double n10 = sa * m00 + ca * m10, n11 = sa * m01 + ca * m11;
+          P[pk_idx(pa, pb, l)] = n00 * cb - n01 * sb;
+          if (rb) P[pk_idx(pa, qb, l)] = n00 * sb + n01 * cb;
+          if (ra) P[pk_idx(qa, pb, l)] = n10 * cb - n11 * sb;
+          if (ra && rb) P[pk_idx(qa, qb, l)] = n10 * sb + n11 * cb;
+        }
+      }
+      // V <- V J  (columns p_b, q_b of every row)
+      for (int idx = tid; idx < l * h; idx += nt) {
+        const int i = idx % l, b = idx / l;
+        if (!act[b]) continue;
+        const int pb = pp[b], qb = qq[b];
+        const double cb = cs[2 * b], sb = cs[2 * b + 1];
+        const double vp = V[i + pb * l], vq = V[i + qb * l];
+        V[i + pb * l] = cb * vp - sb * vq;
+        V[i + qb * l] = sb * vp + cb * vq;
+      }
+      __syncthreads();
+    }
+    if (!rotated) { converged = true; break; }
+  }
+  __syncthreads();
+  // sort eigenvalues descending (rank by counting; ties by index)
+  for (int i = tid; i < l; i += nt) {
+    const double li = P[pk_idx(i, i, l)];
+    int rank = 0;
+    for (int j = 0; j < l; ++j) {
+      const double lj = P[pk_idx(j, j, l)];
+      rank += (lj > li) || (lj == li && j < i);
+    }
+    sigma[rank] = sqrt(fmax(li, 0.0));
+    for (int r = 0; r < l; ++r) UB[r + (int64_t)rank * l] = V[r + i * l];
+  }
+  if (tid == 0) {
+    *sweeps_out = converged ? sweep + 1 : sweep;
+    if (!converged) atomicOr(flags, FLAG_NOCONV);
+  }
+}
+
+// ---- shrinkage and the l x l factors of Eq. (6) ----------------------------
+// wmode: 0 tau (scalar: tau_dev ? *tau_dev : tau), 1 explicit w (device, l),
+//        2 reciprocal C/(sigma+eps), 3 reweighted C/(d_prev+eps) (falls back
+//        to 2 when no previous call).
+// Kept set K = {i : d_i > 0} (compacted, ascending). Outputs (ld l):
+//   Mc[:, j] = U_B[:, K_j]            (carry Q~ = Q Mc, Alg. 1 line 21)
+//   Mp[:, j] = U_B[:, K_j] * d_{K_j}/sigma_{K_j}   (so Wt = B^T Mp = V_K diag(d))
+// and the report vector rep = {sigma[l], d[l]}; ints {r, flags}.
+template <typename Tq>
+__global__ void shrink_kernel(const double* __restrict__ sigma, const double* __restrict__ UB,
+                              int l, const int* __restrict__ s_dev, int wmode, double tau,
+                              const double* __restrict__ tau_dev, const double* __restrict__ w,
+                              double C, double eps, double* __restrict__ d_prev, int* have_prev,
+                              Tq* __restrict__ Mc, Tq* __restrict__ Mp, int* __restrict__ r_dev,
+                              int* __restrict__ flags, double* __restrict__ rep) {
+  __shared__ double d_sh[FRSVT_LMAX], f_sh[FRSVT_LMAX];
+  __shared__ int kept[FRSVT_LMAX];
+  __shared__ int r_sh;
+  const int tid = threadIdx.x;
+  const int s = *s_dev;
+  const int prev_ok = *have_prev;
+  for (int i = tid; i < l; i += blockDim.x) {
+    const double sg = sigma[i];
+    double t;
+    if (wmode == 0) t = tau_dev ? *tau_dev : tau;
+    else if (wmode == 1) t = w[i];
+    else if (wmode == 3 && prev_ok) t = C / (d_prev[i] + eps);
+    else t = C / (sg + eps);
+    double d = (i < s) ? fmax(sg - t, 0.0) : 0.0;
+    if (!isfinite(d)) d = 0.0;
+    d_sh[i] = d;
+    f_sh[i] = (d > 0.0 && sg > 0.0) ? d / sg : 0.0;
+    rep[i] = sg;
+    rep[FRSVT_LMAX + i] = d;
+    if (wmode == 1 && i + 1 < l && w[i + 1] < w[i]) atomicOr(flags, FLAG_NONMONOTONE_W);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int r = 0;
+    for (int i = 0; i < l; ++i)
+      if (d_sh[i] > 0.0) kept[r++] = i;
+    r_sh = r;
+    *r_dev = r;
+    *have_prev = 1;
+  }
+  __syncthreads();
+  for (int i = tid; i < l; i += blockDim.x) d_prev[i] = d_sh[i];
+  const int r = r_sh;
+  for (int idx = tid; idx < l * l; idx += blockDim.x) {
+    const int row = idx % l, j = idx / l;
+    double vc = 0.0, vp = 0.0;
+    if (j < r) {
+      const int src = kept[j];
+      vc = UB[row + (int64_t)src * l];
+      vp = vc * f_sh[src];
+    }
+    Mc[idx] = (Tq)vc;
+    Mp[idx] = (Tq)vp;
+  }
+}
+
+// ---- reductions over an m x n column-major matrix --------------------------
+template <typename T>
+__global__ void absmax_sumsq_kernel(const T* __restrict__ X, int64_t m, int64_t n, int64_t ld,
+                                    double* __restrict__ part_max, double* __restrict__ part_ss) {
+  __shared__ double scratch[32];
+  double mx = 0.0, ss = 0.0;
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m, j = idx / m;
+    const double v = (double)X[i + j * ld];
+    mx = fmax(mx, fabs(v));
+    ss += v * v;
+  }
+  const double bm = block_max(mx, scratch);
+  const double bs = block_sum(ss, scratch);
+  if (threadIdx.x == 0) { part_max[blockIdx.x] = bm; part_ss[blockIdx.x] = bs; }
+}
+
+// single block: fold partial maxima / sums (fixed order)
+__global__ void fold_kernel(const double* __restrict__ part_max, const double* __restrict__ part_ss,
+                            int nparts, double* __restrict__ out_max, double* __restrict__ out_ss) {
+  __shared__ double scratch[32];
+  double mx = 0.0, ss = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    if (part_max) mx = fmax(mx, part_max[i]);
+    if (part_ss) ss += part_ss[i];
+  }
+  mx = block_max(mx, scratch);
+  ss = block_sum(ss, scratch);
+  if (threadIdx.x == 0) {
+    if (out_max) *out_max = mx;
+    if (out_ss) *out_ss = ss;
+  }
+}
+
+// ALM scalars after the init reductions:
+//   norm2 = supplied or sqrt(lambda_max) of the block-power estimate,
+//   mu0 = supplied or 1.25/norm2, mu_bar = factor*mu0,
+//   J = max(norm2, ||D||_inf / lambda); scal = {mu0, mu_bar, 1/J, norm2, ||D||_F^2 ...}
+__global__ void alm_scalars_kernel(double norm2_supplied, const double* __restrict__ sigma_est,
+                                   double mu0_supplied, double mu_factor, double lambda,
+                                   const double* __restrict__ dmax, double* __restrict__ mu,
+                                   double* __restrict__ scal) {
+  const double n2 = norm2_supplied > 0.0 ? norm2_supplied : sigma_est[0];
+  const double mu0 = mu0_supplied > 0.0 ? mu0_supplied : 1.25 / n2;
+  mu[0] = mu0;
+  mu[1] = mu_factor * mu0;
+  const double J = fmax(n2, *dmax / lambda);
+  scal[0] = 1.0 / J;
+  scal[1] = n2;
+}
+
+// E_1 = S_{lambda/mu_0}(D + Y_0/mu_0), A_1 = D - E_1 + Y_0/mu_0 with Y_0 = D/J
+// (L_0 = E_0 = 0).
+template <typename T>
+__global__ void alm_init_kernel(const T* __restrict__ D, T* __restrict__ E, T* __restrict__ A,
+                                int64_t m, int64_t n, int64_t ld, const double* __restrict__ mu,
+                                const double* __restrict__ scal, double lambda) {
+  const double mu0 = mu[0];
+  const T yscale = (T)(scal[0] / mu0);  // (1/J)/mu0
+  const T thr = (T)(lambda / mu0);
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (idx % m) + (idx / m) * ld;
+    const T d = D[o];
+    const T y = d * yscale;
+    const T e = soft<T>(d + y, thr);
+    E[o] = e;
+    A[o] = d - e + y;
+  }
+}
+
+// after the fused ALM epilogue: fold the residual partials (local sum)
+__global__ void fold_sum_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) ss += part[i];
+  ss = block_sum(ss, scratch);
+  if (threadIdx.x == 0) *out = ss;
+}
+
+// relative residual ||D - L - E||_F / ||D||_F and mu_{k+1} = min(rho mu_k, mu_bar)
+__global__ void alm_mu_kernel(double rho, int finalize, double* __restrict__ mu,
+                              const double* __restrict__ dss, double* __restrict__ resid) {
+  resid[1] = sqrt(resid[0] / fmax(*dss, 1e-300));
+  if (!finalize) mu[0] = fmin(rho * mu[0], mu[1]);
+}
+
+// tau = 1/mu (device) for the SVT of the ALM step
+__global__ void tau_from_mu_kernel(const double* __restrict__ mu, double* __restrict__ tau) {
+  *tau = 1.0 / mu[0];
+}
+
+}  // namespace frsvt

@@ -1,0 +1,115 @@
+"""GPU parity of rpca_alm_step (fused iALM epilogue) against the textbook
+oracle iALM: teacher-forced steps (per-step L within
+1e-4, residual within 1e-3 relative) and free-running recovery (BASELINE:
+RPCA recovery error matches the oracle's within 1e-3 after a fixed count)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_config, omega
+from tests.gpu_util import cm, np64, z14
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1509_00296_b200 as P
+    return P
+
+
+def _run_gpu(P, cfg, D, norm2, n_iter, rho=1.5):
+    m, n = D.shape
+    h = P.Frsvt(m, n, cfg.l, cfg.q, rp=cfg.rp, dtype=torch.float32, seed=cfg.seed)
+    E = torch.empty_like(D)
+    A = torch.empty_like(D)
+    L = torch.empty_like(D)
+    st = h.rpca_state(D, E, A, L, rho=rho, norm2_D=norm2)
+    resid = []
+    for k in range(n_iter):
+        resid.append(h.rpca_step(st, finalize=(k == n_iter - 1), want_resid=True))
+    return h, L, E, resid
+
+
+@pytest.mark.parametrize("name,over", [("c2", {}),
+                                       ("c3", dict(m=96 * 128, n=60, H=96, W=128, nblocks=2, iters=30)),
+                                       ("c5", dict(m=6144, n=768, rank=24, l=40, iters=30,
+                                                   var=1.0 / 6144))])
+def test_rpca_free_running(P, name, over):
+    cfg, d = make_config(name, **over)
+    D = cm(d["D"], torch.float32)
+    D64 = np64(D)
+    L0 = d["L0"].numpy()
+    n2 = oracle.norm2_power(D64)
+    ref = oracle.rpca_ialm(D64, cfg.iters, cfg.l, cfg.q, lambda k: omega(cfg.seed, k, cfg.n, cfg.l).numpy(),
+                           rp=cfg.rp, norm2=n2, L0=L0, rho=cfg.params["rho"])
+    h, L, E, resid = _run_gpu(P, cfg, D, n2, cfg.iters, rho=cfg.params["rho"])
+    Lg = np64(L)
+    nrmse_g = np.linalg.norm(Lg - L0) / np.linalg.norm(L0)
+    nrmse_o = ref["hist"]["nrmse"][-1]
+    assert abs(nrmse_g - nrmse_o) <= 1e-3
+    assert np.linalg.norm(Lg - ref["L"]) <= 1e-3 * np.linalg.norm(ref["L"])
+    # residual reaches the textbook value or the fp32 floor (~u32 * sqrt(mn) relative)
+    assert resid[-1] <= max(10 * ref["hist"]["resid"][-1], 2e-7)
+    assert np.linalg.norm(np64(E) - ref["E"]) <= 1e-3 * np.linalg.norm(ref["E"])
+
+
+def test_rpca_teacher_forced(P):
+    """At every iteration k the GPU gets the oracle's state (E_{k+1}, A_k, mu_k,
+    carry, Omega call index) and its finalize step must reproduce L_{k+1}."""
+    cfg, d = make_config("c2", m=640, n=420, rank=20, l=40, iters=24)
+    D = cm(d["D"], torch.float32)
+    D64 = np64(D)
+    n2 = oracle.norm2_power(D64)
+    ref = oracle.rpca_ialm(D64, cfg.iters, cfg.l, cfg.q, lambda k: omega(cfg.seed, k, cfg.n, cfg.l).numpy(),
+                           norm2=n2, record_states=True)
+    m, n = D.shape
+    h = P.Frsvt(m, n, cfg.l, cfg.q, rp=True, dtype=torch.float32, seed=cfg.seed)
+    E = torch.empty_like(D)
+    A = torch.empty_like(D)
+    L = torch.empty_like(D)
+    st = h.rpca_state(D, E, A, L, norm2_D=n2)
+    h.rpca_step(st, finalize=True)  # init (computes ||D||_F for the residual)
+    mu0 = ref["mu0"]
+    lam = ref["lam"]
+    for k in range(0, cfg.iters, 3):
+        s = ref["states"][k]
+        E.copy_(cm(s["E"], torch.float32))
+        A.copy_(cm(s["A"], torch.float32))
+        h.set_mu(s["mu"], 1e7 * mu0)
+        h.set_carry(None if s["carry"] is None else torch.from_numpy(s["carry"]))
+        h.set_call_index(k)
+        st.iter = k + 1
+        res = h.rpca_step(st, finalize=True, want_resid=True)
+        exp = oracle.frsvt(s["A"], s["Omega"], cfg.l, cfg.q, tau=1.0 / s["mu"], carry=s["carry"], rp=True)
+        assert z14(L, exp.X, s["A"]) <= 1e-4, k
+        r_exp = np.linalg.norm(D64 - exp.X - s["E"]) / np.linalg.norm(D64)
+        assert abs(res - r_exp) <= 1e-3 * r_exp + 1e-7, k
+        # the non-finalize step advances mu and rewrites (E, A) as the textbook update
+        st.iter = k + 1
+        h.set_carry(None if s["carry"] is None else torch.from_numpy(s["carry"]))
+        h.set_call_index(k)
+        h.rpca_step(st, finalize=False)
+        mu1 = min(1.5 * s["mu"], 1e7 * mu0)
+        assert abs(h.get_mu() - mu1) <= 1e-12 * mu1
+        Y1 = s["mu"] * (s["A"] - exp.X)   # Y_{k+1} = mu_k (A_k - L_{k+1})
+        Enext = oracle.soft_shrink(D64 - exp.X + Y1 / mu1, lam / mu1)
+        Anext = D64 - Enext + Y1 / mu1
+        assert np.linalg.norm(np64(E) - Enext) <= 2e-4 * max(np.linalg.norm(Enext), 1e-3 * np.linalg.norm(D64)), k
+        assert np.linalg.norm(np64(A) - Anext) <= 2e-4 * np.linalg.norm(Anext), k
+
+
+def test_rpca_c2_trajectory(P):
+    """BASELINE c2 at full size: r = 0 early, planted rank 50 at the end."""
+    cfg, d = make_config("c2")
+    D = cm(d["D"], torch.float32)
+    n2 = oracle.norm2_power(np64(D))
+    h, L, E, resid = _run_gpu(P, cfg, D, n2, cfg.iters)
+    info = h.info()
+    assert info.r == 50
+    assert resid[-1] <= 1e-6
+    L0 = d["L0"].numpy()
+    assert np.linalg.norm(np64(L) - L0) / np.linalg.norm(L0) <= 1e-4
