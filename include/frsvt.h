@@ -169,6 +169,14 @@ frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar);
 /* Number of kernels this handle has launched since creation (host counter). */
 int64_t frsvt_kernel_launches(const frsvt_handle* h);
 
+/* Test hook: one streaming pass with a chosen implementation (synchronises).
+ * kind 0: out (m_local x l, ld m_local) = A (m_local x n) * B (n x l, ld n)
+ * kind 1: out (n x l, ld n) = A^T * B (m_local x l, ld m_local), summed over ranks
+ * impl 0 = SIMT CUDA cores, 1 = tcgen05 3xTF32 (fp32 handles; needs lda % 4 == 0
+ * and a 16-byte aligned A, otherwise the SIMT path runs). */
+frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                              const void* B, void* out);
+
 /* Pass profiling: with enable != 0 every kernel that streams the m x n
  * operand is bracketed by CUDA events on the handle's stream (enabling resets
  * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,

@@ -213,6 +213,24 @@ class Frsvt:
     def set_mu(self, mu, mu_bar):
         _check("rpca_set_mu", lib.rpca_set_mu(self._h, float(mu), float(mu_bar)))
 
+    def debug_pass(self, kind, impl, A, B):
+        """kind 0: A @ B (m x l); kind 1: A.T @ B (n x l). impl 0 SIMT, 1 tcgen05."""
+        lda = _ld(A, self.m, self.dtype, "A")
+        if kind == 0:
+            B = colmajor(B)
+            _ld(B, self.n, self.dtype, "B")
+            out = torch.empty((self.l, self.m), dtype=self.dtype, device=A.device).t()
+        else:
+            B = colmajor(B)
+            _ld(B, self.m, self.dtype, "B")
+            out = torch.empty((self.l, self.n), dtype=self.dtype, device=A.device).t()
+        if B.stride(1) != B.shape[0]:
+            B = B.t().contiguous().t()
+        _check("frsvt_debug_pass", lib.frsvt_debug_pass(self._h, int(kind), int(impl), ctypes.c_void_p(A.data_ptr()),
+                                                        lda, ctypes.c_void_p(B.data_ptr()),
+                                                        ctypes.c_void_p(out.data_ptr())))
+        return out
+
     def profile(self, enable=True):
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 

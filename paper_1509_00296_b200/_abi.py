@@ -14,7 +14,7 @@ SYMBOLS = [
     "frsvt_apply", "frsvt_apply_weighted", "rpca_alm_step", "frsvt_set_omega",
     "frsvt_draw_omega", "frsvt_get_carry", "frsvt_set_carry", "frsvt_reset_carry",
     "frsvt_set_call_index", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
-    "frsvt_kernel_launches", "frsvt_profile", "frsvt_profile_read",
+    "frsvt_kernel_launches", "frsvt_profile", "frsvt_profile_read", "frsvt_debug_pass",
 ]
 
 
@@ -66,6 +66,7 @@ def load_library(path=LIB_PATH):
         "rpca_set_mu": (i32, [vp, dbl, dbl]),
         "frsvt_kernel_launches": (i64, [vp]),
         "frsvt_profile": (i32, [vp, i32]),
+        "frsvt_debug_pass": (i32, [vp, i32, i32, vp, i64, vp, vp]),
         "frsvt_profile_read": (i32, [vp, i32, P(dbl), P(i64), P(dbl)]),
     }
     for name, (res, args) in sig.items():

@@ -14,11 +14,14 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "small.cuh"
+#include "tc_pass.cuh"
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -54,6 +57,10 @@ struct frsvt_handle {
   void *Om, *OmOv, *Y, *Q, *Qtmp, *Qt, *Z, *Zq, *Zt, *Wt;
   void *T1, *Mc, *Mp;
   double *wvec;
+  // tcgen05 path (fp32): tf32 hi/lo splits of the small operands (ld padded to 4)
+  float *Xh, *Xl, *Qh, *Ql;
+  int64_t ldxs, ldqs;
+  int use_tc;
   void* partq;       // split-K partials of A^T Q (dtype)
   size_t partq_elems;
   double* partd;     // Gram split-K partials (fp64)
@@ -216,6 +223,100 @@ int atq_splits(int64_t n, int64_t rows, int l) {
   return (int)s;
 }
 
+// ---------------------------------------------------------------- tcgen05 glue
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool tma_encode_available() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return true;
+}
+
+// 2-D fp32 tensor map over a column-major matrix (dim0 contiguous, ld elements)
+bool make_map(CUtensorMap* map, const float* ptr, uint64_t dim0, uint64_t dim1, uint64_t ld, uint32_t box0,
+              uint32_t box1, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool tc_eligible(const frsvt_handle* h, const void* A, int64_t lda) {
+  return h->use_tc && h->esz == 4 && h->l >= 16 && (lda % 4) == 0 && ((uintptr_t)A % 16) == 0;
+}
+
+int tc_np(int l) { return l <= 32 ? 32 : (l <= 64 ? 64 : 128); }
+
+template <int MODE, int NP>
+frsvt_status launch_tc_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                          int Mtot, int Ktot, int splits, float* out, int64_t ldo, int64_t zstride,
+                          const float* add, int64_t ldadd) {
+  const size_t smem = tc::PassSmem::total(NP);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(tc::tc_pass_kernel<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int nchunks = (int)cdiv(Ktot, tc::BK);
+  const int cps = (int)cdiv(nchunks, splits);
+  dim3 grid((unsigned)cdiv(Mtot, 128), (unsigned)splits);
+  tc::tc_pass_kernel<MODE, NP><<<grid, tc::PASS_THREADS, smem, h->st>>>(mA, mBh, mBl, Mtot, Ktot, cps, h->l, out, ldo, zstride,
+                                                           add, ldadd);
+  return post_launch(h);
+}
+
+template <int MODE>
+frsvt_status launch_tc(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                       int Mtot, int Ktot, int splits, float* out, int64_t ldo, int64_t zstride, const float* add,
+                       int64_t ldadd) {
+  const int np = tc_np(h->l);
+  if (np == 32) return launch_tc_np<MODE, 32>(h, mA, mBh, mBl, Mtot, Ktot, splits, out, ldo, zstride, add, ldadd);
+  if (np == 64) return launch_tc_np<MODE, 64>(h, mA, mBh, mBl, Mtot, Ktot, splits, out, ldo, zstride, add, ldadd);
+  return launch_tc_np<MODE, 128>(h, mA, mBh, mBl, Mtot, Ktot, splits, out, ldo, zstride, add, ldadd);
+}
+
+frsvt_status split_small(frsvt_handle* h, const float* X, int64_t rows, int64_t ldx, float* Hi, float* Lo,
+                         int64_t ldo) {
+  tc::split_tf32_kernel<<<grid1d(rows * h->l), 256, 0, h->st>>>(X, rows, h->l, ldx, Hi, Lo, ldo);
+  return post_launch(h);
+}
+
+// Y (m x l) = A X (+ Add) on tensor cores (3xTF32)
+frsvt_status tc_AX(frsvt_handle* h, const float* A, int64_t lda, const float* X, float* Y, const float* Add) {
+  TRY(split_small(h, X, h->n, h->n, h->Xh, h->Xl, h->ldxs));
+  const uint32_t np = (uint32_t)tc_np(h->l);
+  CUtensorMap mA, mBh, mBl;
+  if (!make_map(&mA, A, h->m, h->n, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map(&mBh, h->Xh, h->n, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBl, h->Xl, h->n, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
+    return FRSVT_ECUDA;
+  return launch_tc<tc::MODE_AX>(h, mA, mBh, mBl, (int)h->m, (int)h->n, 1, Y, h->m, 0, Add, h->m);
+}
+
+// partials of Z (n x l) = A^T Q on tensor cores, split-K over rows
+frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q, float* part, int splits) {
+  TRY(split_small(h, Q, h->m, h->m, h->Qh, h->Ql, h->ldqs));
+  const uint32_t np = (uint32_t)tc_np(h->l);
+  CUtensorMap mA, mBh, mBl;
+  if (!make_map(&mA, A, h->m, h->n, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBh, h->Qh, h->m, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBl, h->Ql, h->m, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
+    return FRSVT_ECUDA;
+  return launch_tc<tc::MODE_ATQ>(h, mA, mBh, mBl, (int)h->n, (int)h->m, splits, part, h->n,
+                                 (int64_t)h->n * h->l, nullptr, 0);
+}
+
 frsvt_status allreduce(frsvt_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
   if (h->cfg.nranks <= 1) return FRSVT_OK;
   CKN(ncclAllReduce(buf, buf, count, t, op, h->comm, h->st));
@@ -272,6 +373,13 @@ frsvt_status orth(frsvt_handle* h, const T* In, int64_t rows, T* Out, T* Tmp, bo
 // Y (m x l) = A (m x n) * X (n x l)  [+ Add]
 template <typename T>
 frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y, const T* Add) {
+  if constexpr (sizeof(T) == 4) {
+    if (tc_eligible(h, A, lda)) {
+      TRY(prof_begin(h));
+      TRY(tc_AX(h, (const float*)A, lda, (const float*)X, (float*)Y, (const float*)Add));
+      return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
+    }
+  }
   TRY(prof_begin(h));
   if (Add) {
     EpiStoreAdd<T> epi{Y, h->m, Add, h->m};
@@ -288,9 +396,20 @@ template <typename T>
 frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z) {
   const int S = atq_splits(h->n, h->m, h->l);
   EpiStore<T> epi{(T*)h->partq, h->n, (int64_t)h->n * h->l};
-  TRY(prof_begin(h));
-  TRY((launch_skinny<T, T, false, true>(h, (int)h->n, h->l, (int)h->m, S, A, lda, Q, h->m, nullptr, epi)));
-  TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
+  bool done = false;
+  if constexpr (sizeof(T) == 4) {
+    if (tc_eligible(h, A, lda)) {
+      TRY(prof_begin(h));
+      TRY(tc_AtQ(h, (const float*)A, lda, (const float*)Q, (float*)h->partq, S));
+      TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
+      done = true;
+    }
+  }
+  if (!done) {
+    TRY(prof_begin(h));
+    TRY((launch_skinny<T, T, false, true>(h, (int)h->n, h->l, (int)h->m, S, A, lda, Q, h->m, nullptr, epi)));
+    TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
+  }
   splitk_reduce_kernel<T, T><<<grid1d(h->n * h->l), 256, 0, h->st>>>((const T*)h->partq, S, (int)h->n, h->l, Z, h->n);
   TRY(post_launch(h));
   TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
@@ -497,7 +616,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -568,7 +687,11 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
                 {(void**)&h->sigma, sizeof(double) * FRSVT_LMAX},
                 {(void**)&h->dprev, sizeof(double) * FRSVT_LMAX},
                 {(void**)&h->redtmp, sizeof(double) * 64},
-                {(void**)&h->dev, sizeof(DevState)}};
+                {(void**)&h->dev, sizeof(DevState)},
+                {(void**)&h->Xh, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->n, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Xl, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->n, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Qh, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->m, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Ql, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->m, 4) * 4 * l * 4 : 16}};
   for (auto& a : allocs) {
     if (cudaMalloc(a.p, a.bytes) != cudaSuccess) {
       cudaGetLastError();
@@ -577,6 +700,12 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     }
   }
   cudaMemset(h->Qt, 0, ml);
+  h->ldxs = cdiv(h->n, 4) * 4;
+  h->ldqs = cdiv(h->m, 4) * 4;
+  {
+    const char* e = getenv("FRSVT_SIMT");
+    h->use_tc = (c.dtype == FRSVT_F32) && !(e && e[0] == '1') && tma_encode_available();
+  }
   cudaMemset(h->dev, 0, sizeof(DevState));
   cudaMemset(h->sigma, 0, sizeof(double) * FRSVT_LMAX);
   cudaMemset(h->dprev, 0, sizeof(double) * FRSVT_LMAX);
@@ -730,6 +859,26 @@ frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar) {
 }
 
 int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : -1; }
+
+frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                              const void* B, void* out) {
+  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 1) return FRSVT_EINVAL;
+  const int saved = h->use_tc;
+  if (impl == 1 && !(h->esz == 4 && tma_encode_available())) return FRSVT_EINVAL;
+  h->use_tc = impl;
+  frsvt_status st;
+  if (h->esz == 4) {
+    st = kind == 0 ? gemm_AX<float>(h, (const float*)A, lda, (const float*)B, (float*)out, nullptr)
+                   : gemm_AtQ<float>(h, (const float*)A, lda, (const float*)B, (float*)out);
+  } else {
+    st = kind == 0 ? gemm_AX<double>(h, (const double*)A, lda, (const double*)B, (double*)out, nullptr)
+                   : gemm_AtQ<double>(h, (const double*)A, lda, (const double*)B, (double*)out);
+  }
+  h->use_tc = saved;
+  if (st != FRSVT_OK) return st;
+  CK(cudaStreamSynchronize(h->st));
+  return FRSVT_OK;
+}
 
 frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable) {
   if (!h) return FRSVT_EINVAL;

@@ -62,6 +62,22 @@ def _u53(x0, x1):
     return ((x0 >> 5).double() * 67108864.0 + (x1 >> 6).double()) * (2.0 ** -53)
 
 
+def uniform_at(seed, stream, e):
+    """fp64 uniforms at arbitrary element indices e (int64 tensor)."""
+    x0, x1, _, _ = _words(seed, stream, e)
+    return _u53(x0, x1)
+
+
+def normal_at(seed, stream, e):
+    """fp64 standard normals at arbitrary element indices e (int64 tensor)."""
+    x0, x1, x2, x3 = _words(seed, stream, e >> 1)
+    ua = _u53(x0, x1)
+    ub = _u53(x2, x3)
+    rad = torch.sqrt(-2.0 * torch.log1p(-ua))
+    ang = (2.0 * math.pi) * ub
+    return torch.where((e & 1) == 0, rad * torch.cos(ang), rad * torch.sin(ang))
+
+
 def uniform(seed, stream, count, device="cpu", start=0):
     """fp64 uniforms in [0,1) for elements start..start+count-1 of a stream."""
     t = torch.arange(start, start + count, dtype=torch.int64, device=device)

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from .philox import normal, uniform
+from .philox import normal, normal_at, uniform, uniform_at
 
 SEED0 = 150900296  # arXiv id 1509.00296
 
@@ -53,11 +53,18 @@ CONFIGS = {
 }
 
 
-def _col_block(gen, seed, stream, rows_total, row0, m_loc, cols, device):
-    """Rows [row0, row0+m_loc) of a rows_total x cols column-major stream."""
+def _col_block(gen, seed, stream, rows_total, row0, m_loc, cols, device, chunk=1 << 25):
+    """Rows [row0, row0+m_loc) of a rows_total x cols column-major stream
+    (element (i, j) is e = i + rows_total*j), generated in column chunks."""
+    at = {normal: normal_at, uniform: uniform_at}[gen]
     out = torch.empty((cols, m_loc), dtype=torch.float64, device=device)
-    for j in range(cols):
-        out[j] = gen(seed, stream, m_loc, device=device, start=row0 + rows_total * j)
+    rows = torch.arange(row0, row0 + m_loc, dtype=torch.int64, device=device)
+    step = max(1, chunk // max(m_loc, 1))
+    for j0 in range(0, cols, step):
+        j1 = min(cols, j0 + step)
+        cj = torch.arange(j0, j1, dtype=torch.int64, device=device)
+        e = rows[None, :] + rows_total * cj[:, None]
+        out[j0:j1] = at(seed, stream, e)
     return out.t()
 
 
