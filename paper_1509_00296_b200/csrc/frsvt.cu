@@ -14,7 +14,9 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "small.cuh"
+#include "small2.cuh"
 #include "tc_pass.cuh"
+#include "tc_compose.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -31,7 +33,7 @@ using namespace frsvt;
 namespace {
 
 struct DevState {
-  int s, r, flags, sweeps, have_prev, pad0, pad1, pad2;
+  int s, r, flags, sweeps, have_prev, s2, pad1, pad2;
   double mu[2];        // mu_k, mu_bar
   double tau;
   double scal[4];      // 1/J, ||D||_2
@@ -59,6 +61,8 @@ struct frsvt_handle {
   double *wvec;
   // tcgen05 path (fp32): tf32 hi/lo splits of the small operands (ld padded to 4)
   float *Xh, *Xl, *Qh, *Ql;
+  float *QtTh, *QtTl, *WtTh, *WtTl;  // K-major (Kp x rows) splits for the composition
+  int Kp;
   int64_t ldxs, ldqs;
   int use_tc;
   void* partq;       // split-K partials of A^T Q (dtype)
@@ -209,7 +213,7 @@ frsvt_status launch_gram_tile(frsvt_handle* h, int l, int K, int splits, const T
 
 int gram_splits(int64_t rows) {
   int64_t s = cdiv(rows, 256);
-  if (s > 296) s = 296;
+  if (s > 148) s = 148;
   if (s < 1) s = 1;
   return (int)s;
 }
@@ -292,29 +296,87 @@ frsvt_status split_small(frsvt_handle* h, const float* X, int64_t rows, int64_t 
   return post_launch(h);
 }
 
-// Y (m x l) = A X (+ Add) on tensor cores (3xTF32)
-frsvt_status tc_AX(frsvt_handle* h, const float* A, int64_t lda, const float* X, float* Y, const float* Add) {
-  TRY(split_small(h, X, h->n, h->n, h->Xh, h->Xl, h->ldxs));
+// Y (M x l, ldy) = A (M x K, lda) X (K x l, ldx) (+ Add) on tensor cores (3xTF32)
+frsvt_status tc_AX_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t M, int64_t K, const float* X,
+                       int64_t ldx, float* Y, int64_t ldy, const float* Add, int64_t ldadd) {
+  TRY(split_small(h, X, K, ldx, h->Xh, h->Xl, h->ldxs));
   const uint32_t np = (uint32_t)tc_np(h->l);
   CUtensorMap mA, mBh, mBl;
-  if (!make_map(&mA, A, h->m, h->n, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map(&mBh, h->Xh, h->n, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mBl, h->Xl, h->n, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
+  if (!make_map(&mA, A, M, K, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map(&mBh, h->Xh, K, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBl, h->Xl, K, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
     return FRSVT_ECUDA;
-  return launch_tc<tc::MODE_AX>(h, mA, mBh, mBl, (int)h->m, (int)h->n, 1, Y, h->m, 0, Add, h->m);
+  return launch_tc<tc::MODE_AX>(h, mA, mBh, mBl, (int)M, (int)K, 1, Y, ldy, 0, Add, ldadd);
+}
+frsvt_status tc_AX(frsvt_handle* h, const float* A, int64_t lda, const float* X, float* Y, const float* Add) {
+  return tc_AX_gen(h, A, lda, h->m, h->n, X, h->n, Y, h->m, Add, h->m);
 }
 
-// partials of Z (n x l) = A^T Q on tensor cores, split-K over rows
-frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q, float* part, int splits) {
-  TRY(split_small(h, Q, h->m, h->m, h->Qh, h->Ql, h->ldqs));
+// partials (splits x Mcols x l) of A^T Q, A (rows x Mcols, lda), Q (rows x l, ldq), split-K over rows
+frsvt_status tc_AtQ_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t rows, int64_t Mcols, const float* Q,
+                        int64_t ldq, float* part, int splits) {
+  TRY(split_small(h, Q, rows, ldq, h->Qh, h->Ql, h->ldqs));
   const uint32_t np = (uint32_t)tc_np(h->l);
   CUtensorMap mA, mBh, mBl;
-  if (!make_map(&mA, A, h->m, h->n, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mBh, h->Qh, h->m, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mBl, h->Ql, h->m, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
+  if (!make_map(&mA, A, rows, Mcols, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBh, h->Qh, rows, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mBl, h->Ql, rows, h->l, h->ldqs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
     return FRSVT_ECUDA;
-  return launch_tc<tc::MODE_ATQ>(h, mA, mBh, mBl, (int)h->n, (int)h->m, splits, part, h->n,
-                                 (int64_t)h->n * h->l, nullptr, 0);
+  return launch_tc<tc::MODE_ATQ>(h, mA, mBh, mBl, (int)Mcols, (int)rows, splits, part, Mcols,
+                                 (int64_t)Mcols * h->l, nullptr, 0);
+}
+frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q, float* part, int splits) {
+  return tc_AtQ_gen(h, A, lda, h->m, h->n, Q, h->m, part, splits);
+}
+
+// tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows) matrix
+bool tc_small_ok(const frsvt_handle* h, int64_t rows) {
+  return h->use_tc && h->esz == 4 && h->l >= 16 && (rows % 4) == 0 && rows >= 128;
+}
+
+// X = Q~ Wt^T fused with its consumer (tc::EPI_*) on tensor cores. Returns the
+// number of residual partials written to h->redpart.
+frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const float* D, float* A, float* E,
+                        int64_t ld, double rho, double lambda, int* nparts) {
+  const int Kp = h->Kp;
+  {
+    dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
+    tc::split_transpose_kernel<<<g1, 256, 0, h->st>>>((const float*)h->Qt, h->m, h->l, h->m, Kp, h->QtTh, h->QtTl);
+    TRY(post_launch(h));
+    dim3 g2((unsigned)cdiv(h->n, 32), (unsigned)(Kp / 32));
+    tc::split_transpose_kernel<<<g2, 256, 0, h->st>>>((const float*)h->Wt, h->n, h->l, h->n, Kp, h->WtTh, h->WtTl);
+    TRY(post_launch(h));
+  }
+  CUtensorMap mQh, mQl, mWh, mWl;
+  if (!make_map(&mQh, h->QtTh, Kp, h->m, Kp, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mQl, h->QtTl, Kp, h->m, Kp, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mWh, h->WtTh, Kp, h->n, Kp, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mWl, h->WtTl, Kp, h->n, Kp, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return FRSVT_ECUDA;
+  const int rbs = (int)cdiv(h->m, 128), ntiles = (int)cdiv(h->n, 128);
+  int cs = rbs >= 2 * 148 ? 1 : (int)cdiv(2 * 148, rbs);
+  if (cs > ntiles) cs = ntiles;
+  const int tpc = (int)cdiv(ntiles, cs);
+  cs = (int)cdiv(ntiles, tpc);
+  dim3 grid((unsigned)rbs, (unsigned)cs);
+  const size_t smem = tc::ComposeSmem::total();
+  static bool attr[3] = {false, false, false};
+#define FRSVT_LAUNCH_CMP(EPIV)                                                                                  \
+  do {                                                                                                          \
+    if (!attr[EPIV]) {                                                                                          \
+      CK(cudaFuncSetAttribute(tc::tc_compose_kernel<EPIV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      attr[EPIV] = true;                                                                                        \
+    }                                                                                                           \
+    tc::tc_compose_kernel<EPIV><<<grid, tc::CMP_THREADS, smem, h->st>>>(mQh, mQl, mWh, mWl, (int)h->m, (int)h->n, \
+                                                                        &h->dev->r, tpc, X, ldx, D, A, E, ld,    \
+                                                                        h->dev->mu, rho, lambda, h->redpart);    \
+  } while (0)
+  if (epi == tc::EPI_STORE) FRSVT_LAUNCH_CMP(tc::EPI_STORE);
+  else if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP(tc::EPI_ALM);
+  else FRSVT_LAUNCH_CMP(tc::EPI_FINAL);
+#undef FRSVT_LAUNCH_CMP
+  if (nparts) *nparts = (int)(grid.x * grid.y);
+  return post_launch(h);
 }
 
 frsvt_status allreduce(frsvt_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
@@ -334,7 +396,8 @@ frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sh
   const int S = gram_splits(rows);
   EpiStore<double> epi{h->partd, l, (int64_t)l * l};
   TRY(launch_gram_tile<T>(h, l, (int)rows, S, Y, ld, epi));
-  splitk_reduce_kernel<double, double><<<grid1d((int64_t)l * l), 256, 0, h->st>>>(h->partd, S, l, l, h->G, l);
+  splitk_reduce_wide_kernel<double, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(h->partd, S, l, l,
+                                                                                                   h->G, l);
   TRY(post_launch(h));
   if (sharded) TRY(allreduce(h, h->G, (size_t)l * l, ncclFloat64, ncclSum));
   return FRSVT_OK;
@@ -344,12 +407,13 @@ template <typename T>
 frsvt_status chol(frsvt_handle* h, T* Tout) {
   const int l = h->l;
   const double tol = sizeof(T) == 4 ? 1e-12 : 1e-13;
-  const size_t smem = ((size_t)l * l + 3 * l) * sizeof(double) + 2 * l * sizeof(int);
-  chol_piv_kernel<T><<<1, 512, smem, h->st>>>(h->G, l, tol, Tout, &h->dev->s, &h->dev->flags);
+  small2_kernel<SM2_ORTH, T><<<1, 1024, small2_smem_bytes(l, SM2_ORTH), h->st>>>(
+      h->G, l, tol, Tout, nullptr, nullptr, &h->dev->s, nullptr, &h->dev->flags, 0);
   return post_launch(h);
 }
 
-// Out (rows x l) = In (rows x l) * M (l x l)
+// Out (rows x l) = In (rows x l) * M (l x l), fp32-accurate SIMT (used where
+// the small factor is ill-conditioned: the first CholeskyQR pass)
 template <typename T>
 frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldin, const T* Msm,
                          T* Out, int64_t ldout) {
@@ -358,15 +422,47 @@ frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldi
                                           nullptr, epi);
 }
 
-// CholeskyQR2 with pivoted truncated Cholesky (reading R4/R5 in DESIGN.md)
+// Out = In * M with a well-conditioned M (orthogonal-like): tensor cores when
+// eligible (3xTF32, ~2e-6 relative), else SIMT
+template <typename T>
+frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, const T* Msm, T* Out) {
+  if constexpr (sizeof(T) == 4) {
+    if (tc_small_ok(h, rows))
+      return tc_AX_gen(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows, nullptr, 0);
+  }
+  return apply_small<T>(h, In, rows, rows, Msm, Out, rows);
+}
+
+// G = Y^T Y of a nearly orthonormal Y (second CholeskyQR pass): tensor cores
+// when eligible (fp32 partials of 3xTF32 products, folded in fp64), else fp64 SIMT
+template <typename T>
+frsvt_status gram_fast(frsvt_handle* h, const T* Y, int64_t rows, bool sharded) {
+  if constexpr (sizeof(T) == 4) {
+    if (tc_small_ok(h, rows)) {
+      const int l = h->l;
+      int S = (int)cdiv(rows, 256);
+      if (S > 296) S = 296;
+      TRY(tc_AtQ_gen(h, (const float*)Y, rows, rows, l, (const float*)Y, rows, (float*)h->partq, S));
+      splitk_reduce_wide_kernel<float, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(
+          (const float*)h->partq, S, l, l, h->G, l);
+      TRY(post_launch(h));
+      if (sharded) TRY(allreduce(h, h->G, (size_t)l * l, ncclFloat64, ncclSum));
+      return FRSVT_OK;
+    }
+  }
+  return gram<T>(h, Y, rows, rows, sharded);
+}
+
+// CholeskyQR2 with pivoted truncated Cholesky (readings R2/R4 in DESIGN.md):
+// pass 1 fp64 Gram + fp32-accurate apply, pass 2 on the nearly orthonormal Q1
 template <typename T>
 frsvt_status orth(frsvt_handle* h, const T* In, int64_t rows, T* Out, T* Tmp, bool sharded) {
   TRY(gram<T>(h, In, rows, rows, sharded));
   TRY(chol<T>(h, (T*)h->T1));
   TRY(apply_small<T>(h, In, rows, rows, (const T*)h->T1, Tmp, rows));
-  TRY(gram<T>(h, Tmp, rows, rows, sharded));
+  TRY(gram_fast<T>(h, Tmp, rows, sharded));
   TRY(chol<T>(h, (T*)h->T1));
-  TRY(apply_small<T>(h, Tmp, rows, rows, (const T*)h->T1, Out, rows));
+  TRY(apply_fast<T>(h, Tmp, rows, (const T*)h->T1, Out));
   return FRSVT_OK;
 }
 
@@ -444,10 +540,8 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda) {
   const int l = h->l;
   TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
   TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
-  const size_t smem = ((size_t)l * (l + 1) / 2 + (size_t)l * l + FRSVT_LMAX) * sizeof(double) +
-                      3 * (FRSVT_LMAX / 2) * sizeof(int);
-  jacobi_eig_kernel<<<1, 1024, smem, h->st>>>(h->G, l, 40, h->sigma, h->UB, &h->dev->sweeps,
-                                               &h->dev->flags);
+  small2_kernel<SM2_EIG, double><<<1, 1024, small2_smem_bytes(l, SM2_EIG), h->st>>>(
+      h->G, l, 4e-15, nullptr, h->sigma, h->UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40);
   return post_launch(h);
 }
 
@@ -460,8 +554,8 @@ frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const do
                                          C, eps, h->dprev, &h->dev->have_prev, (T*)h->Mc, (T*)h->Mp,
                                          &h->dev->r, &h->dev->flags, h->dev->rep);
   TRY(post_launch(h));
-  TRY(apply_small<T>(h, (const T*)h->Q, h->m, h->m, (const T*)h->Mc, (T*)h->Qt, h->m));
-  TRY(apply_small<T>(h, (const T*)h->Z, h->n, h->n, (const T*)h->Mp, (T*)h->Wt, h->n));
+  TRY(apply_fast<T>(h, (const T*)h->Q, h->m, (const T*)h->Mc, (T*)h->Qt));
+  TRY(apply_fast<T>(h, (const T*)h->Z, h->n, (const T*)h->Mp, (T*)h->Wt));
   return FRSVT_OK;
 }
 
@@ -478,6 +572,13 @@ frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, dou
 // X = Q~ Wt^T  (reconstruction, K = r)
 template <typename T>
 frsvt_status compose_X(frsvt_handle* h, T* X, int64_t ldx) {
+  if constexpr (sizeof(T) == 4) {
+    if (h->use_tc) {
+      TRY(prof_begin(h));
+      TRY(tc_compose(h, tc::EPI_STORE, (float*)X, ldx, nullptr, nullptr, nullptr, 0, 0.0, 0.0, nullptr));
+      return prof_end(h, 2, (double)h->m * h->n * sizeof(T));
+    }
+  }
   EpiStore<T> epi{X, ldx, 0};
   TRY(prof_begin(h));
   TRY((launch_tile<T, T, 128, 128, 16, 8, 8, true, false>(h, (int)h->m, (int)h->n, h->l, 1,
@@ -559,14 +660,24 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   TRY(post_launch(h));
   TRY(frsvt_core<T>(h, A, st->ld, 0, 0.0, &h->dev->tau, 0.0, 0.0));
   // fused reconstruction + iALM epilogue (one pass over D, A, E)
-  const int gx = (int)cdiv(h->m, 128), gy = (int)cdiv(h->n, 128);
-  EpiAlm<T> epi{D, A, E, (T*)st->L, st->ld, h->dev->mu, st->rho, lambda, finalize, h->redpart};
+  int nparts = (int)(cdiv(h->m, 128) * cdiv(h->n, 128));
   TRY(prof_begin(h));
-  TRY((launch_tile<T, T, 128, 128, 16, 8, 8, true, false>(h, (int)h->m, (int)h->n, h->l, 1,
-                                                         (const T*)h->Qt, h->m, (const T*)h->Wt, h->n,
-                                                         &h->dev->r, epi)));
+  bool done = false;
+  if constexpr (sizeof(T) == 4) {
+    if (h->use_tc) {
+      TRY(tc_compose(h, finalize ? tc::EPI_FINAL : tc::EPI_ALM, (float*)st->L, st->ld, (const float*)D, (float*)A,
+                     (float*)E, st->ld, st->rho, lambda, &nparts));
+      done = true;
+    }
+  }
+  if (!done) {
+    EpiAlm<T> epi{D, A, E, (T*)st->L, st->ld, h->dev->mu, st->rho, lambda, finalize, h->redpart};
+    TRY((launch_tile<T, T, 128, 128, 16, 8, 8, true, false>(h, (int)h->m, (int)h->n, h->l, 1,
+                                                           (const T*)h->Qt, h->m, (const T*)h->Wt, h->n,
+                                                           &h->dev->r, epi)));
+  }
   TRY(prof_end(h, 2, (double)h->m * h->n * sizeof(T) * (finalize ? 3.0 : 5.0)));
-  fold_sum_kernel<<<1, 256, 0, h->st>>>(h->redpart, gx * gy, &h->dev->resid[0]);
+  fold_sum_kernel<<<1, 256, 0, h->st>>>(h->redpart, nparts, &h->dev->resid[0]);
   TRY(post_launch(h));
   TRY(allreduce(h, &h->dev->resid[0], 1, ncclFloat64, ncclSum));
   alm_mu_kernel<<<1, 1, 0, h->st>>>(st->rho, finalize, h->dev->mu, &h->dev->dss, h->dev->resid);
@@ -581,9 +692,8 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
 
 template <typename T>
 void set_smem_attrs() {
-  const int l = FRSVT_LMAX;
-  const size_t chol_smem = ((size_t)l * l + 3 * l) * sizeof(double) + 2 * l * sizeof(int);
-  cudaFuncSetAttribute(chol_piv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
+  cudaFuncSetAttribute(small2_kernel<SM2_ORTH, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)small2_smem_bytes(FRSVT_LMAX, SM2_ORTH));
 }
 
 }  // namespace
@@ -616,7 +726,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -667,6 +777,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   const size_t ml = (size_t)h->m * l * h->esz, nl = (size_t)h->n * l * h->esz, ll = (size_t)l * l * h->esz;
   const int S_atq = atq_splits(h->n, h->m, l);
   h->partq_elems = (size_t)S_atq * h->n * l;
+  if (h->partq_elems < (size_t)296 * l * l) h->partq_elems = (size_t)296 * l * l;
   const int64_t maxrows = h->m > h->n ? h->m : h->n;
   h->partd_elems = (size_t)gram_splits(maxrows) * l * l;
   const int64_t gx = cdiv(h->m, 128), gy = cdiv(h->n, 128);
@@ -688,10 +799,14 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
                 {(void**)&h->dprev, sizeof(double) * FRSVT_LMAX},
                 {(void**)&h->redtmp, sizeof(double) * 64},
                 {(void**)&h->dev, sizeof(DevState)},
-                {(void**)&h->Xh, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->n, 4) * 4 * l * 4 : 16},
-                {(void**)&h->Xl, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->n, 4) * 4 * l * 4 : 16},
-                {(void**)&h->Qh, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->m, 4) * 4 * l * 4 : 16},
-                {(void**)&h->Ql, c.dtype == FRSVT_F32 ? (size_t)cdiv(h->m, 4) * 4 * l * 4 : 16}};
+                {(void**)&h->Xh, c.dtype == FRSVT_F32 ? (size_t)cdiv(maxrows, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Xl, c.dtype == FRSVT_F32 ? (size_t)cdiv(maxrows, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Qh, c.dtype == FRSVT_F32 ? (size_t)cdiv(maxrows, 4) * 4 * l * 4 : 16},
+                {(void**)&h->Ql, c.dtype == FRSVT_F32 ? (size_t)cdiv(maxrows, 4) * 4 * l * 4 : 16},
+                {(void**)&h->QtTh, c.dtype == FRSVT_F32 ? (size_t)h->m * cdiv(l, 32) * 32 * 4 : 16},
+                {(void**)&h->QtTl, c.dtype == FRSVT_F32 ? (size_t)h->m * cdiv(l, 32) * 32 * 4 : 16},
+                {(void**)&h->WtTh, c.dtype == FRSVT_F32 ? (size_t)h->n * cdiv(l, 32) * 32 * 4 : 16},
+                {(void**)&h->WtTl, c.dtype == FRSVT_F32 ? (size_t)h->n * cdiv(l, 32) * 32 * 4 : 16}};
   for (auto& a : allocs) {
     if (cudaMalloc(a.p, a.bytes) != cudaSuccess) {
       cudaGetLastError();
@@ -700,8 +815,9 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     }
   }
   cudaMemset(h->Qt, 0, ml);
-  h->ldxs = cdiv(h->n, 4) * 4;
-  h->ldqs = cdiv(h->m, 4) * 4;
+  h->ldxs = cdiv(maxrows, 4) * 4;
+  h->Kp = (int)cdiv(l, 32) * 32;
+  h->ldqs = cdiv(maxrows, 4) * 4;
   {
     const char* e = getenv("FRSVT_SIMT");
     h->use_tc = (c.dtype == FRSVT_F32) && !(e && e[0] == '1') && tma_encode_available();
@@ -711,11 +827,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   cudaMemset(h->dprev, 0, sizeof(double) * FRSVT_LMAX);
   set_smem_attrs<float>();
   set_smem_attrs<double>();
-  {
-    const size_t jsmem = ((size_t)FRSVT_LMAX * (FRSVT_LMAX + 1) / 2 + (size_t)FRSVT_LMAX * FRSVT_LMAX +
-                          FRSVT_LMAX) * sizeof(double) + 3 * (FRSVT_LMAX / 2) * sizeof(int);
-    cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsmem);
-  }
+  cudaFuncSetAttribute(small2_kernel<SM2_EIG, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)small2_smem_bytes(FRSVT_LMAX, SM2_EIG));
   if (c.nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, 128);

@@ -74,6 +74,30 @@ __global__ void splitk_reduce_kernel(const Tp* __restrict__ part, int S, int M, 
   }
 }
 
+// split-K reduction for few outputs / many partials: each block owns 32
+// consecutive outputs, its 8 warps stride over z (coalesced 128-byte rows),
+// a fixed-order shared-memory fold => deterministic.
+template <typename Tp, typename Tout>
+__global__ void __launch_bounds__(256) splitk_reduce_wide_kernel(const Tp* __restrict__ part, int S, int M, int N,
+                                                                 Tout* __restrict__ C, int64_t ldc) {
+  __shared__ double acc[8][33];
+  const int64_t MN = (int64_t)M * N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (idx < MN)
+    for (int z = warp; z < S; z += 8) s += (double)part[z * MN + idx];
+  acc[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && idx < MN) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += acc[w][lane];
+    const int i = (int)(idx % M), j = (int)(idx / M);
+    C[i + (int64_t)j * ldc] = (Tout)t;
+  }
+}
+
 // ---- pivoted truncated Cholesky (single CTA, fp64, matrix in shared mem) ---
 // Input : G (l x l fp64 Gram, column-major, ld l).
 // Output: T (l x l, ld l) with Y*T = orth(Y) restricted to the revealed rank s:
@@ -393,18 +417,31 @@ __global__ void shrink_kernel(const double* __restrict__ sigma, const double* __
 }
 
 // ---- reductions over an m x n column-major matrix --------------------------
+// (4 consecutive rows per thread when the layout allows 16-byte loads)
 template <typename T>
 __global__ void absmax_sumsq_kernel(const T* __restrict__ X, int64_t m, int64_t n, int64_t ld,
                                     double* __restrict__ part_max, double* __restrict__ part_ss) {
   __shared__ double scratch[32];
   double mx = 0.0, ss = 0.0;
-  const int64_t total = m * n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % m, j = idx / m;
-    const double v = (double)X[i + j * ld];
-    mx = fmax(mx, fabs(v));
-    ss += v * v;
+  const bool vec = sizeof(T) == 4 && (m % 4) == 0 && (ld % 4) == 0 && ((uintptr_t)X % 16) == 0;
+  if (vec) {
+    const int64_t m4 = m / 4, total = m4 * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i4 = idx % m4, j = idx / m4;
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X) + j * ld) + i4);
+      mx = fmax(mx, fmax(fmax(fabs((double)v.x), fabs((double)v.y)), fmax(fabs((double)v.z), fabs((double)v.w))));
+      ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+  } else {
+    const int64_t total = m * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = idx % m, j = idx / m;
+      const double v = (double)X[i + j * ld];
+      mx = fmax(mx, fabs(v));
+      ss += v * v;
+    }
   }
   const double bm = block_max(mx, scratch);
   const double bs = block_sum(ss, scratch);
@@ -454,6 +491,25 @@ __global__ void alm_init_kernel(const T* __restrict__ D, T* __restrict__ E, T* _
   const double mu0 = mu[0];
   const T yscale = (T)(scal[0] / mu0);  // (1/J)/mu0
   const T thr = (T)(lambda / mu0);
+  const bool vec = sizeof(T) == 4 && (m % 4) == 0 && (ld % 4) == 0 && ((uintptr_t)D % 16) == 0 &&
+                   ((uintptr_t)E % 16) == 0 && ((uintptr_t)A % 16) == 0;
+  if (vec) {
+    const int64_t m4 = m / 4, total = m4 * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = (idx % m4) * 4 + (idx / m4) * ld;
+      const float4 d = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(D) + o));
+      float4 e, a;
+      const float ys = (float)yscale, th = (float)thr;
+      e.x = soft<float>(d.x + d.x * ys, th); a.x = d.x - e.x + d.x * ys;
+      e.y = soft<float>(d.y + d.y * ys, th); a.y = d.y - e.y + d.y * ys;
+      e.z = soft<float>(d.z + d.z * ys, th); a.z = d.z - e.z + d.z * ys;
+      e.w = soft<float>(d.w + d.w * ys, th); a.w = d.w - e.w + d.w * ys;
+      __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(E) + o), e);
+      __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(A) + o), a);
+    }
+    return;
+  }
   const int64_t total = m * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
