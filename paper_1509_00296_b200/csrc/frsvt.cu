@@ -15,6 +15,7 @@
 #include "gemm_simt.cuh"
 #include "small.cuh"
 #include "small2.cuh"
+#include "orth_chol.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
 
@@ -407,8 +408,8 @@ template <typename T>
 frsvt_status chol(frsvt_handle* h, T* Tout) {
   const int l = h->l;
   const double tol = sizeof(T) == 4 ? 1e-12 : 1e-13;
-  small2_kernel<SM2_ORTH, T><<<1, 1024, small2_smem_bytes(l, SM2_ORTH), h->st>>>(
-      h->G, l, tol, Tout, nullptr, nullptr, &h->dev->s, nullptr, &h->dev->flags, 0);
+  orth_chol_kernel<T><<<1, OC_THREADS, orth_chol_smem_bytes(l), h->st>>>(h->G, l, tol, Tout, &h->dev->s,
+                                                                          &h->dev->flags);
   return post_launch(h);
 }
 
@@ -540,8 +541,11 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda) {
   const int l = h->l;
   TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
   TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
-  small2_kernel<SM2_EIG, double><<<1, 1024, small2_smem_bytes(l, SM2_EIG), h->st>>>(
-      h->G, l, 4e-15, nullptr, h->sigma, h->UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40);
+  // rotation threshold: fp64 handles converge to 1e-15 (parity 1e-10), fp32 to
+  // 1e-10 relative off-orthogonality (far below the 1e-4 parity bar)
+  const double jtol = h->esz == 8 ? 1e-15 : 1e-10;
+  small2_kernel<SM2_EIG, double><<<1, SM2_THREADS, small2_smem_bytes(l, SM2_EIG), h->st>>>(
+      h->G, l, 4e-15, nullptr, h->sigma, h->UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40, jtol);
   return post_launch(h);
 }
 
@@ -692,8 +696,8 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
 
 template <typename T>
 void set_smem_attrs() {
-  cudaFuncSetAttribute(small2_kernel<SM2_ORTH, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)small2_smem_bytes(FRSVT_LMAX, SM2_ORTH));
+  cudaFuncSetAttribute(orth_chol_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)orth_chol_smem_bytes(FRSVT_LMAX));
 }
 
 }  // namespace
