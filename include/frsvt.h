@@ -177,6 +177,17 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h);
 frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                               const void* B, void* out);
 
+/* Test hook: the small SVD (Alg. 1 lines 16-18, reading Z8) alone, on an
+ * l x l fp64 Gram G = B B^T (device, column-major, ld l; NULL = the Gram the
+ * handle's last call decomposed). impl 0 is the production kernel (one-sided
+ * Jacobi on G), 1 a two-sided Jacobi, 2 pivoted Cholesky + one-sided Jacobi
+ * on the factor (earlier kernels, kept for comparison). Gcopy (device, nullable) receives the
+ * Gram used. Outputs: sigma (device, l values, descending), UB (device, l x l,
+ * ld l), *sweeps (host, nullable) and, when reps > 0, the mean device time of
+ * `reps` back-to-back launches (*ms, host). Synchronises. */
+frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* G, double* Gcopy, double* sigma,
+                                   double* UB, int32_t* sweeps, int32_t reps, double* ms);
+
 /* Pass profiling: with enable != 0 every kernel that streams the m x n
  * operand is bracketed by CUDA events on the handle's stream (enabling resets
  * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,

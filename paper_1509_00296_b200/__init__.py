@@ -231,6 +231,25 @@ class Frsvt:
                                                         ctypes.c_void_p(out.data_ptr())))
         return out
 
+    def debug_small_svd(self, impl=0, G=None, reps=0):
+        """Small SVD of an l x l fp64 Gram (None = the last call's Gram).
+        Returns (sigma, UB, G_used, sweeps, mean_ms)."""
+        l = self.l
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if G is not None:
+            G = G.to(device=dev, dtype=torch.float64).t().contiguous().t()
+            if tuple(G.shape) != (l, l):
+                raise ValueError("G must be %d x %d" % (l, l))
+        Gc = torch.empty((l, l), dtype=torch.float64, device=dev).t()
+        sig = torch.empty(l, dtype=torch.float64, device=dev)
+        UB = torch.empty((l, l), dtype=torch.float64, device=dev).t()
+        sw, ms = ctypes.c_int32(), ctypes.c_double()
+        _check("frsvt_debug_small_svd", lib.frsvt_debug_small_svd(
+            self._h, int(impl), ctypes.c_void_p(G.data_ptr() if G is not None else 0),
+            ctypes.c_void_p(Gc.data_ptr()), ctypes.c_void_p(sig.data_ptr()), ctypes.c_void_p(UB.data_ptr()),
+            ctypes.byref(sw), int(reps), ctypes.byref(ms)))
+        return sig, UB, Gc, sw.value, ms.value
+
     def profile(self, enable=True):
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 

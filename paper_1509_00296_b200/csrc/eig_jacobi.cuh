@@ -1,0 +1,429 @@
+// Small SVD of B from its l x l fp64 Gram G = B B^T (Alg. 1 lines 16-18,
+// reading Z8): a single-CTA one-sided (Hestenes) Jacobi on the columns of G
+// itself, register resident.
+//
+// G is symmetric positive semidefinite, so a rotation sequence V that makes
+// the columns of M = G V mutually orthogonal gives G V = V Lambda: the
+// column norms are lambda_i = sigma_i(B)^2 and the normalised columns are the
+// left singular vectors U_B. (The Gram already carries the squared condition
+// number; factoring it first, e.g. by Cholesky, adds no accuracy and costs a
+// serial l-step phase, so the sweep runs on G directly.)
+//
+// Parallel ordering: the round-robin "circle" tournament on L2 (even) column
+// positions, L2 - 1 rounds per sweep, L2/2 disjoint pairs per round: T[0]
+// stays, the ring T[1] -> ... -> T[h-1] -> B[h-1] -> ... -> B[0] -> T[1]
+// advances one position per round, and pair q is (T[q], B[q]). Column c >= 1
+// starts at ring index c - 1, so the column in every slot at every round is
+// a closed form (eig_col_at). Warp w owns the 4 pairs q = 4w .. 4w + 3; lane
+// j holds rows j, j+32, j+64, j+96 of its 8 columns in registers. Advancing
+// the ring is a register shift inside a warp; only two columns per warp cross
+// to a neighbour warp, through a double-buffered shared-memory mailbox (one
+// block barrier per round).
+//
+// Per round and warp: 4 partial dots, a reduce-scatter that leaves the dot of
+// pair p in lanes 8p .. 8p+7, the rotation parameters of the 4 pairs computed
+// lane-parallel, then the rotations. Rotations are applied in scaled form
+// (column c is stored as x~ with true column d_c x~): x~' = x~ - a y~,
+// y~' = y~ + b x~ with a = t d_y / d_x, b = t d_x / d_y, d' = c d — two FMAs
+// per element pair instead of four. The per-column metadata (true squared
+// norm, d, 1/d) lives in shared memory indexed by column, so it never moves.
+// Scales are folded back into the data at the start of every sweep, where the
+// norms are also recomputed exactly.
+//
+// A pair rotates when |g| > tol_rot sqrt(|m_p|^2 |m_q|^2), g = m_p . m_q.
+// The solve stops after a sweep with no rotation, or (tol_stop > 0) after a
+// sweep whose largest relative off-diagonal was <= tol_stop: Jacobi sweeps
+// converge quadratically, so the sweep that measured tol_stop leaves
+// off-diagonals near tol_stop^2 (fp32 handles: tol_stop 1e-5 -> ~1e-10).
+//
+// Exact shortcut (t_mode != 0): if the Gershgorin bound max_i sum_j |G_ij| is
+// <= t_min^2, every sigma_i <= t_min and every shrunk value
+// max(sigma_i - t_i, 0) is zero, so the thresholded result (X = 0, r = 0) is
+// known without the decomposition; sigma then reports sqrt(G_ii) (each
+// <= t_min), U_B the matching unit vectors, sweeps 0.
+#pragma once
+#include "common.cuh"
+
+namespace frsvt {
+
+constexpr int EIG_PPW = 4;  // pairs per warp
+
+struct EigJacobi {
+  static int warps(int l) {
+    const int per = 2 * EIG_PPW;
+    return (l + per - 1) / per;
+  }
+  // mailbox [2][nw][2][128] + metadata [128][4] + a/b [nw][4][2]
+  static size_t smem_bytes(int l) {
+    const int nw = warps(l);
+    return ((size_t)2 * nw * 2 * 128 + (size_t)FRSVT_LMAX * 4 + (size_t)nw * EIG_PPW * 2) * sizeof(double) + 64;
+  }
+};
+
+__device__ __forceinline__ double eig_rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double eig_rsqrt_approx(double x) {
+  double r;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+// column in slot T[q] (top) / B[q] (bottom) at round k
+__device__ __forceinline__ int eig_col_at(bool top, int q, int k, int L2) {
+  const int R = L2 - 1;
+  if (top && q == 0) return 0;
+  const int rho = top ? q - 1 : L2 - 2 - q;
+  int c = rho - (k % R);
+  if (c < 0) c += R;
+  return c + 1;
+}
+
+__global__ void __launch_bounds__(512, 1)
+eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict__ t_dev, double t_host,
+                  int t_mode, double tol_rot, double tol_stop, int max_sweeps, double* __restrict__ sigma,
+                  double* __restrict__ UB, int* __restrict__ sweeps_out, int* __restrict__ flags) {
+  constexpr int PPW = EIG_PPW;
+  extern __shared__ double esm[];
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = nw * PPW;  // pairs per round
+  const int L2 = 2 * h;    // positions (>= l; columns >= l are empty)
+  double* mbox = esm;                                // [2][nw][2][128]
+  double* meta = esm + (size_t)2 * nw * 2 * 128;     // [128][4]: N (true |col|^2), d, 1/d, -
+  double* abuf = meta + (size_t)FRSVT_LMAX * 4;      // [nw][PPW][2]: a, b of this round
+  __shared__ double red_d[16];
+  __shared__ int red_i[16];
+  __shared__ int stop_sh, early_sh;
+
+  // ---- exact shortcut: Gershgorin bound vs the smallest threshold --------
+  double t2 = -1.0;
+  if (t_mode == 1) t2 = t_host * t_host;
+  if (t_mode == 2) t2 = (*t_dev) * (*t_dev);
+  {
+    double rs = 0.0;
+    int bad = 0;
+    for (int c = warp; c < l; c += nw) {
+      double a = 0.0;
+      for (int i = lane; i < l; i += 32) a += fabs(G[i + (size_t)c * l]);
+      a = warp_sum(a);
+      rs = fmax(rs, a);
+      if (lane == 0 && !isfinite(G[c + (size_t)c * l])) bad = 1;
+    }
+    if (lane == 0) red_d[warp] = rs;
+    if (bad) atomicOr(flags, FLAG_NONFINITE);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = 0.0;
+      for (int w = 0; w < nw; ++w) mx = fmax(mx, red_d[w]);
+      early_sh = (t2 >= 0.0 && mx <= t2) ? 1 : 0;
+    }
+    __syncthreads();
+  }
+  if (early_sh) {
+    for (int c = threadIdx.x; c < l; c += blockDim.x) {
+      const double gc = fmax(G[c + (size_t)c * l], 0.0);
+      int rank = 0;
+      for (int j = 0; j < l; ++j) {
+        const double gj = fmax(G[j + (size_t)j * l], 0.0);
+        rank += (gj > gc) || (gj == gc && j < c);
+      }
+      sigma[rank] = sqrt(gc);
+      for (int i = 0; i < l; ++i) UB[i + (size_t)rank * l] = (i == c) ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) *sweeps_out = 0;
+    return;
+  }
+
+  // ---- load (round-0 placement of the closed form) ------------------------
+  double x[PPW][4], y[PPW][4];  // stored top / bottom slot columns
+  const int q0 = warp * PPW;
+#pragma unroll
+  for (int j = 0; j < PPW; ++j) {
+    const int ct = eig_col_at(true, q0 + j, 0, L2), cb = eig_col_at(false, q0 + j, 0, L2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = lane + 32 * e;
+      const double vx = (ct < l && i < l) ? G[i + (size_t)ct * l] : 0.0;
+      const double vy = (cb < l && i < l) ? G[i + (size_t)cb * l] : 0.0;
+      x[j][e] = isfinite(vx) ? vx : 0.0;
+      y[j][e] = isfinite(vy) ? vy : 0.0;
+    }
+  }
+  for (int c = threadIdx.x; c < FRSVT_LMAX; c += blockDim.x) {
+    meta[4 * c + 0] = 0.0;
+    meta[4 * c + 1] = 1.0;
+    meta[4 * c + 2] = 1.0;
+    meta[4 * c + 3] = 0.0;
+  }
+
+  const double tol2 = tol_rot * tol_rot;
+  const int pj = lane >> 3;  // the pair this lane computes parameters for
+  const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+  int sweep = 0;
+  bool converged = false;
+  int rnd_base = 0;  // rounds elapsed (ring offset)
+  for (; sweep < max_sweeps; ++sweep) {
+    __syncthreads();  // metadata of the previous sweep complete
+    // fold the scales into the data and recompute exact norms
+    {
+      double a[2 * PPW];
+#pragma unroll
+      for (int j = 0; j < PPW; ++j) {
+        const int ct = eig_col_at(true, q0 + j, rnd_base, L2), cb = eig_col_at(false, q0 + j, rnd_base, L2);
+        const double dxv = meta[4 * ct + 1], dyv = meta[4 * cb + 1];
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[j][e] *= dxv;
+          y[j][e] *= dyv;
+          s0 = fma(x[j][e], x[j][e], s0);
+          s1 = fma(y[j][e], y[j][e], s1);
+        }
+        a[2 * j] = s0;
+        a[2 * j + 1] = s1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 2 * PPW; ++j) a[j] += __shfl_xor_sync(0xffffffffu, a[j], o);
+      __syncthreads();  // every warp has read the old scales
+      if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < PPW; ++j) {
+          const int ct = eig_col_at(true, q0 + j, rnd_base, L2), cb = eig_col_at(false, q0 + j, rnd_base, L2);
+          meta[4 * ct + 0] = ct < l ? a[2 * j] : 0.0;
+          meta[4 * ct + 1] = 1.0;
+          meta[4 * ct + 2] = 1.0;
+          meta[4 * cb + 0] = cb < l ? a[2 * j + 1] : 0.0;
+          meta[4 * cb + 1] = 1.0;
+          meta[4 * cb + 2] = 1.0;
+        }
+      }
+      __syncthreads();
+    }
+    double maxrel = 0.0;
+    int rotated = 0;
+    // ring indices of this lane's parameter pair, advanced by one per round
+    const int Rr = L2 - 1;
+    int rho_x = (q0 + pj == 0) ? -1 : q0 + pj - 1, rho_y = L2 - 2 - (q0 + pj);
+    {
+      const int k = rnd_base % Rr;
+      if (rho_x >= 0) rho_x = (rho_x - k + Rr) % Rr;
+      rho_y = (rho_y - k + Rr) % Rr;
+    }
+    for (int rr = 0; rr < L2 - 1; ++rr) {
+      const int rnd = rnd_base + rr;
+      // partial dots, then a reduce-scatter: the 8-lane group p ends with the
+      // full (stored) dot of pair p
+      double gp[PPW];
+#pragma unroll
+      for (int j = 0; j < PPW; ++j) {
+        double s = x[j][0] * y[j][0];
+#pragma unroll
+        for (int e = 1; e < 4; ++e) s = fma(x[j][e], y[j][e], s);
+        gp[j] = s;
+      }
+      double k0 = b4 ? gp[2] : gp[0], k1 = b4 ? gp[3] : gp[1];
+      k0 += __shfl_xor_sync(0xffffffffu, b4 ? gp[0] : gp[2], 16);
+      k1 += __shfl_xor_sync(0xffffffffu, b4 ? gp[1] : gp[3], 16);
+      double gm = b3 ? k1 : k0;
+      gm += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+      gm += __shfl_xor_sync(0xffffffffu, gm, 4);
+      gm += __shfl_xor_sync(0xffffffffu, gm, 2);
+      gm += __shfl_xor_sync(0xffffffffu, gm, 1);
+      // rotation parameters of pair pj, lane-parallel over the 4 pairs
+      {
+        const int cx = rho_x + 1, cy = rho_y + 1;  // column = (ring index - round) mod R, + 1
+        if (rho_x >= 0) rho_x = (rho_x == 0) ? Rr - 1 : rho_x - 1;
+        rho_y = (rho_y == 0) ? Rr - 1 : rho_y - 1;
+        const double2 mx01 = *reinterpret_cast<const double2*>(meta + 4 * cx);
+        const double2 my01 = *reinterpret_cast<const double2*>(meta + 4 * cy);
+        const double dinx = meta[4 * cx + 2], diny = meta[4 * cy + 2];
+        const double al = mx01.x, be = my01.x, dxv = mx01.y, dyv = my01.y;
+        const double g = gm * dxv * dyv;  // true dot
+        const double abv = al * be, gg = g * g;
+        double a = 0.0, b = 0.0;
+        const bool rot = (cx < l) && (cy < l) && al > 0.0 && be > 0.0 && gg > tol2 * abv;
+        if (rot) {
+          maxrel = fmax(maxrel, gg * eig_rcp_approx(abv));
+          // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
+          // to ~1e-7 relative: any t defines an exact rotation once c, s are
+          // consistent with it, an approximate angle only leaves a ~1e-7 fraction
+          // of g for the next sweep
+          const double zeta = 0.5 * (be - al) * eig_rcp_approx(g);
+          const double az = fmin(fabs(zeta), 1e150);
+          const double z1 = fma(az, az, 1.0);
+          const double tt = eig_rcp_approx(az + z1 * eig_rsqrt_approx(z1));
+          const double t = zeta >= 0.0 ? tt : -tt;
+          // c = 1/sqrt(1 + t^2) to full precision (two Newton steps)
+          const double q1 = fma(t, t, 1.0);
+          double c = eig_rsqrt_approx(q1);
+          c = c * fma(-0.5 * q1 * c, c, 1.5);
+          c = c * fma(-0.5 * q1 * c, c, 1.5);
+          const double s = c * t, ic = q1 * c;  // ic = 1/c
+          a = t * dyv * dinx;
+          b = t * dxv * diny;
+          rotated = 1;
+          if ((lane & 7) == 0) {
+            const double c2 = c * c, s2 = s * s, cs2 = 2.0 * c * s * g;
+            meta[4 * cx + 0] = fma(c2, al, fma(s2, be, -cs2));
+            meta[4 * cx + 1] = c * dxv;
+            meta[4 * cx + 2] = ic * dinx;
+            meta[4 * cy + 0] = fma(s2, al, fma(c2, be, cs2));
+            meta[4 * cy + 1] = c * dyv;
+            meta[4 * cy + 2] = ic * diny;
+          }
+        }
+        if ((lane & 7) == 0) {
+          abuf[(warp * PPW + pj) * 2 + 0] = a;
+          abuf[(warp * PPW + pj) * 2 + 1] = b;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < PPW; ++j) {
+        const double2 abj = *reinterpret_cast<const double2*>(abuf + (warp * PPW + j) * 2);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double xv = x[j][e], yv = y[j][e];
+          x[j][e] = fma(-abj.x, yv, xv);
+          y[j][e] = fma(abj.y, xv, yv);
+        }
+      }
+      // ---- advance the ring by one position -------------------------------
+      double* mb = mbox + (size_t)(rnd & 1) * nw * 2 * 128;
+      if (warp + 1 < nw) {  // last top slot -> warp + 1
+        double* outT = mb + (size_t)(warp * 2 + 0) * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) outT[32 * e + lane] = x[PPW - 1][e];
+      }
+      if (warp > 0) {  // first bottom slot -> warp - 1
+        double* outB = mb + (size_t)(warp * 2 + 1) * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) outB[32 * e + lane] = y[0][e];
+      }
+      double tmp[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tmp[e] = y[0][e];
+#pragma unroll
+      for (int j = 0; j < PPW - 1; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[j][e] = y[j + 1][e];
+      if (warp == nw - 1) {  // T[h-1] -> B[h-1]
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[PPW - 1][e] = x[PPW - 1][e];
+      }
+#pragma unroll
+      for (int j = PPW - 1; j >= 2; --j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[j][e] = x[j - 1][e];
+      if (warp == 0) {  // T[0] stays, B[0] -> T[1]
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[1][e] = tmp[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[1][e] = x[0][e];
+      }
+      __syncthreads();
+      if (warp > 0) {  // T[q0] <- warp - 1's last top slot
+        const double* inT = mb + (size_t)((warp - 1) * 2 + 0) * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[0][e] = inT[32 * e + lane];
+      }
+      if (warp + 1 < nw) {  // B[q0 + PPW - 1] <- warp + 1's first bottom slot
+        const double* inB = mb + (size_t)((warp + 1) * 2 + 1) * 128;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[PPW - 1][e] = inB[32 * e + lane];
+      }
+    }
+    rnd_base += L2 - 1;
+    // ---- sweep verdict -----------------------------------------------------
+    maxrel = warp_max(maxrel);
+    rotated = __any_sync(0xffffffffu, rotated);
+    if (lane == 0) {
+      red_d[warp] = maxrel;
+      red_i[warp] = rotated;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mr = 0.0;
+      int any = 0;
+      for (int w = 0; w < nw; ++w) {
+        mr = fmax(mr, red_d[w]);
+        any |= red_i[w];
+      }
+      stop_sh = (!any) || (tol_stop > 0.0 && mr <= tol_stop * tol_stop);
+    }
+    __syncthreads();
+    if (stop_sh) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+
+  // ---- sigma = sqrt(d |x~|), U_B = x~ / |x~|, sorted descending ------------
+  __syncthreads();
+  double nrm[2 * PPW];
+#pragma unroll
+  for (int j = 0; j < PPW; ++j) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s0 = fma(x[j][e], x[j][e], s0);
+      s1 = fma(y[j][e], y[j][e], s1);
+    }
+    nrm[j] = s0;
+    nrm[PPW + j] = s1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int j = 0; j < 2 * PPW; ++j) nrm[j] += __shfl_xor_sync(0xffffffffu, nrm[j], o);
+  double* lam = mbox;  // reuse the mailbox: lambda per column
+  int cols[2 * PPW];
+  double lams[2 * PPW];
+#pragma unroll
+  for (int j = 0; j < 2 * PPW; ++j) {
+    const int c = eig_col_at(j < PPW, q0 + (j < PPW ? j : j - PPW), rnd_base, L2);
+    cols[j] = c;
+    nrm[j] = sqrt(nrm[j]);
+    lams[j] = (c < l) ? fabs(meta[4 * c + 1]) * nrm[j] : 0.0;
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 2 * PPW; ++j)
+      if (cols[j] < l) lam[cols[j]] = lams[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 2 * PPW; ++j) {
+    const int c = cols[j];
+    if (c >= l) continue;
+    const double lc = lams[j];
+    int rank = 0;
+    for (int k = lane; k < l; k += 32) {
+      const double lk = lam[k];
+      rank += (lk > lc) || (lk == lc && k < c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    const double inv = nrm[j] > 0.0 ? 1.0 / nrm[j] : 0.0;
+    if (lane == 0) sigma[rank] = sqrt(lc);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = lane + 32 * e;
+      if (i < l) UB[i + (size_t)rank * l] = ((j < PPW) ? x[j][e] : y[j - PPW][e]) * inv;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *sweeps_out = sweep;
+    if (!converged) atomicOr(flags, FLAG_NOCONV);
+  }
+}
+
+}  // namespace frsvt

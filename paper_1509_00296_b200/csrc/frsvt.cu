@@ -15,6 +15,7 @@
 #include "gemm_simt.cuh"
 #include "small.cuh"
 #include "small2.cuh"
+#include "eig_jacobi.cuh"
 #include "orth_chol.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
@@ -535,18 +536,51 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   return FRSVT_OK;
 }
 
-// B^T = A^T Q, G = B B^T, Jacobi -> sigma, U_B   (Alg. 1 lines 16-18)
-template <typename T>
-frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda) {
+size_t jacobi_eig_smem_bytes(int l) {
+  return ((size_t)l * (l + 1) / 2 + (size_t)l * l + FRSVT_LMAX) * sizeof(double) + 3 * (FRSVT_LMAX / 2) * sizeof(int);
+}
+
+// small SVD of the l x l fp64 Gram G (reading Z8). impl 0: production
+// (register-resident one-sided Jacobi on G, eig_jacobi.cuh); 1: two-sided
+// Jacobi reference; 2: pivoted Cholesky + one-sided Jacobi (small2.cuh);
+// t_mode 0: no shortcut, 1: scalar
+// threshold t_host, 2: scalar threshold *t_dev (exact Gershgorin early-out).
+frsvt_status launch_eig_jacobi(frsvt_handle* h, const double* G, double* sigma, double* UB, int t_mode,
+                               double t_host, const double* t_dev) {
   const int l = h->l;
-  TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
-  TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
-  // rotation threshold: fp64 handles converge to 1e-15 (parity 1e-10), fp32 to
-  // 1e-10 relative off-orthogonality (far below the 1e-4 parity bar)
+  const int nw = EigJacobi::warps(l);
+  const size_t smem = EigJacobi::smem_bytes(l);
+  // fp64 handles: rotate down to 1e-15 relative, confirm with a clean sweep;
+  // fp32 handles: rotate to 1e-9, stop after a sweep that measured <= 1e-5
+  const double tol_rot = h->esz == 8 ? 1e-15 : 1e-9;
+  const double tol_stop = h->esz == 8 ? 0.0 : 1e-5;
+  eig_jacobi_kernel<<<1, 32 * nw, smem, h->st>>>(G, l, t_dev, t_host, t_mode, tol_rot, tol_stop, 40, sigma, UB,
+                                                 &h->dev->sweeps, &h->dev->flags);
+  return post_launch(h);
+}
+
+frsvt_status launch_eig(frsvt_handle* h, int impl, const double* G, double* sigma, double* UB, int t_mode = 0,
+                        double t_host = 0.0, const double* t_dev = nullptr) {
+  const int l = h->l;
+  if (impl == 0) return launch_eig_jacobi(h, G, sigma, UB, t_mode, t_host, t_dev);
+  if (impl == 1) {
+    jacobi_eig_kernel<<<1, 1024, jacobi_eig_smem_bytes(l), h->st>>>(G, l, 40, sigma, UB, &h->dev->sweeps,
+                                                                   &h->dev->flags);
+    return post_launch(h);
+  }
   const double jtol = h->esz == 8 ? 1e-15 : 1e-10;
   small2_kernel<SM2_EIG, double><<<1, SM2_THREADS, small2_smem_bytes(l, SM2_EIG), h->st>>>(
-      h->G, l, 4e-15, nullptr, h->sigma, h->UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40, jtol);
+      G, l, 4e-15, nullptr, sigma, UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40, jtol);
   return post_launch(h);
+}
+
+// B^T = A^T Q, G = B B^T, Jacobi -> sigma, U_B   (Alg. 1 lines 16-18)
+template <typename T>
+frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0, double t_host = 0.0,
+                       const double* t_dev = nullptr) {
+  TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
+  TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
+  return launch_eig(h, 0, h->G, h->sigma, h->UB, t_mode, t_host, t_dev);
 }
 
 // shrink + factors: Q~ = Q Mc, Wt = B^T Mp (Eq. 6 with the kept set)
@@ -567,7 +601,11 @@ template <typename T>
 frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, double tau,
                         const double* tau_dev, double C, double eps) {
   TRY(range_finder<T>(h, A, lda, h->q, 1000u, h->rp != 0, h->call));
-  TRY(small_svd<T>(h, A, lda));
+  // exact early-out of the small SVD when every sigma is certified <= the
+  // smallest threshold (scalar tau, or the smallest explicit weight)
+  if (wmode == 0) TRY(small_svd<T>(h, A, lda, tau_dev ? 2 : 1, tau, tau_dev));
+  else if (wmode == 1) TRY(small_svd<T>(h, A, lda, 1, tau));
+  else TRY(small_svd<T>(h, A, lda));
   TRY(shrink_and_factors<T>(h, wmode, tau, tau_dev, C, eps));
   h->call++;
   return FRSVT_OK;
@@ -615,7 +653,11 @@ template <typename T>
 frsvt_status apply_impl(frsvt_handle* h, const void* A, int64_t lda, int wmode, double tau,
                         const double* w_host, double C, double eps, void* X, int64_t ldx,
                         frsvt_info* info) {
-  if (wmode == 1) CK(cudaMemcpyAsync(h->wvec, w_host, sizeof(double) * h->l, cudaMemcpyHostToDevice, h->st));
+  if (wmode == 1) {
+    CK(cudaMemcpyAsync(h->wvec, w_host, sizeof(double) * h->l, cudaMemcpyHostToDevice, h->st));
+    tau = w_host[0];  // smallest explicit threshold (the small SVD's exact early-out)
+    for (int i = 1; i < h->l; ++i) tau = fmin(tau, w_host[i]);
+  }
   CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
   TRY(frsvt_core<T>(h, (const T*)A, lda, wmode, tau, nullptr, C, eps));
   TRY(compose_X<T>(h, (T*)X, ldx));
@@ -833,6 +875,10 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   set_smem_attrs<double>();
   cudaFuncSetAttribute(small2_kernel<SM2_EIG, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)small2_smem_bytes(FRSVT_LMAX, SM2_EIG));
+  cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)jacobi_eig_smem_bytes(FRSVT_LMAX));
+  cudaFuncSetAttribute(eig_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)EigJacobi::smem_bytes(FRSVT_LMAX));
   if (c.nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, 128);
@@ -994,6 +1040,33 @@ frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const
   h->use_tc = saved;
   if (st != FRSVT_OK) return st;
   CK(cudaStreamSynchronize(h->st));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* G, double* Gcopy, double* sigma,
+                                   double* UB, int32_t* sweeps, int32_t reps, double* ms) {
+  if (!h || !sigma || !UB || impl < 0 || impl > 2 || reps < 0) return FRSVT_EINVAL;
+  const size_t gb = sizeof(double) * h->l * h->l;
+  if (G) CK(cudaMemcpyAsync(h->G, G, gb, cudaMemcpyDeviceToDevice, h->st));
+  if (Gcopy) CK(cudaMemcpyAsync(Gcopy, h->G, gb, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  TRY(launch_eig(h, impl, h->G, sigma, UB));
+  if (reps > 0) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->st));
+    for (int i = 0; i < reps; ++i) TRY(launch_eig(h, impl, h->G, sigma, UB));
+    CK(cudaEventRecord(e1, h->st));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    if (ms) *ms = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  CK(cudaStreamSynchronize(h->st));
+  if (sweeps) CK(cudaMemcpy(sweeps, &h->dev->sweeps, sizeof(int), cudaMemcpyDeviceToHost));
   return FRSVT_OK;
 }
 
