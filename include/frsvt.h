@@ -172,10 +172,17 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h);
 /* Test hook: one streaming pass with a chosen implementation (synchronises).
  * kind 0: out (m_local x l, ld m_local) = A (m_local x n) * B (n x l, ld n)
  * kind 1: out (n x l, ld n) = A^T * B (m_local x l, ld m_local), summed over ranks
- * impl 0 = SIMT CUDA cores, 1 = tcgen05 3xTF32 (fp32 handles; needs lda % 4 == 0
- * and a 16-byte aligned A, otherwise the SIMT path runs). */
+ * impl 0 = SIMT CUDA cores, 1 = tcgen05 3xTF32, 2 = persistent stream-K tcgen05
+ * (fp32 handles; needs lda % 4 == 0 and a 16-byte aligned A, otherwise the
+ * SIMT path runs). */
 frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                               const void* B, void* out);
+/* Same pass `reps` times back to back on the handle's stream (no host sync
+ * in between), *ms = mean device time per pass (CUDA events). impl as above;
+ * impl 2 is the persistent stream-K pass, 3..5 and 8..71 are bandwidth and
+ * pipeline probes of it (outputs not meaningful). Synchronises. */
+frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                                    const void* B, void* out, int32_t reps, double* ms);
 
 /* Test hook: the small SVD (Alg. 1 lines 16-18, reading Z8) alone, on an
  * l x l fp64 Gram G = B B^T (device, column-major, ld l; NULL = the Gram the

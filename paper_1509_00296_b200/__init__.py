@@ -250,6 +250,21 @@ class Frsvt:
             ctypes.byref(sw), int(reps), ctypes.byref(ms)))
         return sig, UB, Gc, sw.value, ms.value
 
+    def debug_pass_timed(self, kind, impl, A, B, reps=10):
+        """Mean device ms of `reps` back-to-back passes (see debug_pass)."""
+        lda = _ld(A, self.m, self.dtype, "A")
+        B = colmajor(B)
+        rows = self.n if kind == 0 else self.m
+        _ld(B, rows, self.dtype, "B")
+        if B.stride(1) != B.shape[0]:
+            B = B.t().contiguous().t()
+        out = torch.empty((self.l, self.m if kind == 0 else self.n), dtype=self.dtype, device=A.device).t()
+        ms = ctypes.c_double()
+        _check("frsvt_debug_pass_timed", lib.frsvt_debug_pass_timed(
+            self._h, int(kind), int(impl), ctypes.c_void_p(A.data_ptr()), lda, ctypes.c_void_p(B.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), int(reps), ctypes.byref(ms)))
+        return ms.value
+
     def profile(self, enable=True):
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 

@@ -19,6 +19,7 @@
 #include "orth_chol.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
+#include "tc_pass2.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -67,6 +68,11 @@ struct frsvt_handle {
   int Kp;
   int64_t ldxs, ldqs;
   int use_tc;
+  int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
+  int nsm;           // SMs of the device (stream-K grid)
+  float* skpart;     // stream-K partial-tile slots (nsm x 2 x 128 x 128 fp32)
+  __nv_bfloat16 *Xb, *Qb;  // bf16 [b_l | b_h] operands of the stream-K passes (ld ldb16)
+  int64_t ldb16;     // leading dimension of the bf16 low parts (multiple of 8)
   void* partq;       // split-K partials of A^T Q (dtype)
   size_t partq_elems;
   double* partd;     // Gram split-K partials (fp64)
@@ -331,6 +337,59 @@ frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q
   return tc_AtQ_gen(h, A, lda, h->m, h->n, Q, h->m, part, splits);
 }
 
+// ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
+template <int MODE, int NP>
+frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0) {
+  const size_t smem = tc::Pass2Smem::total();
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(tc::tc_pass2_kernel<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int mtiles = (int)cdiv(Mtot, 128);
+  const int64_t total = (int64_t)mtiles * cdiv(Ktot, tc::BK);
+  const int G = (int)(total < h->nsm ? total : h->nsm);
+  tc::tc_pass2_kernel<MODE, NP><<<G, tc::P2_THREADS, smem, h->st>>>(mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo,
+                                                                    add, ldadd, h->skpart, dbg);
+  TRY(post_launch(h));
+  if (dbg & 96) return FRSVT_OK;
+  tc::tc_fixup_kernel<NP><<<mtiles, 256, 0, h->st>>>(Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd);
+  return post_launch(h);
+}
+
+// out (Mtot x l) = op(A) * B, B (Ktot x l, ld ldb) the small operand:
+// MODE_AX: A is Mtot x Ktot (lda); MODE_ATQ: A is Ktot x Mtot (lda), op = ^T.
+template <int MODE>
+frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
+                      int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0) {
+  float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
+  __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
+  const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
+  const int64_t kx = cdiv(Ktot, tc::BK) * 2 * tc::BK;  // rows of the bf16 [b_l | b_h] operand
+  tc::split_tf32_bf16x2_kernel<<<grid1d(kx * h->l), 256, 0, h->st>>>(B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
+  TRY(post_launch(h));
+  CUtensorMap mA, mBh, mBl;
+  const uint32_t nb = (uint32_t)h->l;
+  bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
+                                  : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)kx, (cuuint64_t)h->l};
+    cuuint64_t strides[1] = {(cuuint64_t)h->ldb16 * 2};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * tc::BK), nb};
+    cuuint32_t es[2] = {1, 1};
+    ok = ok && g_encode(&mBl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)Bl, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!ok) return FRSVT_ECUDA;
+  const int np = tc_np(h->l);
+  if (np == 32) return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
+  if (np == 64) return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
+  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
+}
+
 // tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows) matrix
 bool tc_small_ok(const frsvt_handle* h, int64_t rows) {
   return h->use_tc && h->esz == 4 && h->l >= 16 && (rows % 4) == 0 && rows >= 128;
@@ -474,7 +533,11 @@ frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y,
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
-      TRY(tc_AX(h, (const float*)A, lda, (const float*)X, (float*)Y, (const float*)Add));
+      if (h->pass2)
+        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)X, h->n, (float*)Y, h->m,
+                                  (const float*)Add, h->m));
+      else
+        TRY(tc_AX(h, (const float*)A, lda, (const float*)X, (float*)Y, (const float*)Add));
       return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
     }
   }
@@ -498,6 +561,13 @@ frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
+      if (h->pass2) {
+        TRY(tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)Q, h->m, (float*)Z, h->n,
+                                   nullptr, 0));
+        TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
+        TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
+        return FRSVT_OK;
+      }
       TRY(tc_AtQ(h, (const float*)A, lda, (const float*)Q, (float*)h->partq, S));
       TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
       done = true;
@@ -742,6 +812,24 @@ void set_smem_attrs() {
                        (int)orth_chol_smem_bytes(FRSVT_LMAX));
 }
 
+// streaming-rate probe of the pass partition (impl 3..5 of frsvt_debug_pass)
+template <int MODE, int SUB>
+frsvt_status probe_stream(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, float* sink) {
+  CUtensorMap mA;
+  const bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
+                                        : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) return FRSVT_ECUDA;
+  const size_t smem = 1024 + (size_t)8 * 128 * tc::BK * 4 + 256;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tc::tma_stream_probe_kernel<MODE, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr = true;
+  }
+  tc::tma_stream_probe_kernel<MODE, SUB><<<h->nsm, 64, smem, h->st>>>(mA, (int)Mtot, (int)Ktot, sink);
+  return post_launch(h);
+}
+
 }  // namespace
 
 // ============================================================== C ABI
@@ -772,7 +860,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -864,6 +952,24 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   h->ldxs = cdiv(maxrows, 4) * 4;
   h->Kp = (int)cdiv(l, 32) * 32;
   h->ldqs = cdiv(maxrows, 4) * 4;
+  h->ldb16 = cdiv(maxrows, tc::BK) * 2 * tc::BK;
+  {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
+    if (nsm > 256) nsm = 256;  // stream-K fixup resolves <= 256 covering CTAs per tile
+    h->nsm = nsm;
+    const char* e = getenv("FRSVT_PASS2");
+    h->pass2 = !(e && e[0] == '0');
+    if (c.dtype == FRSVT_F32 &&
+        (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
+         cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
+         cudaMalloc((void**)&h->Qb, (size_t)h->ldb16 * l * 2) != cudaSuccess)) {
+      cudaGetLastError();
+      free_handle(h);
+      return FRSVT_ENOMEM;
+    }
+  }
   {
     const char* e = getenv("FRSVT_SIMT");
     h->use_tc = (c.dtype == FRSVT_F32) && !(e && e[0] == '1') && tma_encode_available();
@@ -1023,12 +1129,40 @@ frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar) {
 
 int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : -1; }
 
-frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
-                              const void* B, void* out) {
-  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 1) return FRSVT_EINVAL;
-  const int saved = h->use_tc;
-  if (impl == 1 && !(h->esz == 4 && tma_encode_available())) return FRSVT_EINVAL;
-  h->use_tc = impl;
+static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                                      const void* B, void* out) {
+  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 143) return FRSVT_EINVAL;
+  if (impl >= 8 && impl <= 135 && h->esz == 4 && tma_encode_available()) {  // pass2 with pipeline parts disabled
+    frsvt_status st = kind == 0 ? tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n,
+                                                       (float*)out, h->m, nullptr, 0, impl - 8)
+                                : tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m,
+                                                        (float*)out, h->n, nullptr, 0, impl - 8);
+    return st;
+  }
+  if (impl >= 140 && impl <= 143 && h->esz == 4) {  // tensor-pipe rate probe, out[0] = cycles per MMA
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(tc::mma_rate_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+      attr = true;
+    }
+    tc::mma_rate_probe_kernel<<<h->nsm, 128, 80 * 1024, h->st>>>(impl - 140, 2000, (float*)out);
+    return post_launch(h);
+  }
+  if (impl >= 3 && h->esz == 4 && tma_encode_available()) {
+    const bool ax = kind == 0;
+    frsvt_status st;
+    if (impl == 3) st = ax ? probe_stream<tc::MODE_AX, 1>(h, (const float*)A, lda, h->m, h->n, (float*)out)
+                           : probe_stream<tc::MODE_ATQ, 1>(h, (const float*)A, lda, h->n, h->m, (float*)out);
+    else if (impl == 4) st = ax ? probe_stream<tc::MODE_AX, 2>(h, (const float*)A, lda, h->m, h->n, (float*)out)
+                                : probe_stream<tc::MODE_ATQ, 2>(h, (const float*)A, lda, h->n, h->m, (float*)out);
+    else st = ax ? probe_stream<tc::MODE_AX, 4>(h, (const float*)A, lda, h->m, h->n, (float*)out)
+                 : probe_stream<tc::MODE_ATQ, 4>(h, (const float*)A, lda, h->n, h->m, (float*)out);
+    return st;
+  }
+  const int saved = h->use_tc, saved2 = h->pass2;
+  if (impl >= 1 && !(h->esz == 4 && tma_encode_available())) return FRSVT_EINVAL;
+  h->use_tc = impl >= 1 ? 1 : 0;
+  h->pass2 = impl == 2 ? 1 : 0;
   frsvt_status st;
   if (h->esz == 4) {
     st = kind == 0 ? gemm_AX<float>(h, (const float*)A, lda, (const float*)B, (float*)out, nullptr)
@@ -1038,9 +1172,8 @@ frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const
                    : gemm_AtQ<double>(h, (const double*)A, lda, (const double*)B, (double*)out);
   }
   h->use_tc = saved;
-  if (st != FRSVT_OK) return st;
-  CK(cudaStreamSynchronize(h->st));
-  return FRSVT_OK;
+  h->pass2 = saved2;
+  return st;
 }
 
 frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* G, double* Gcopy, double* sigma,
@@ -1067,6 +1200,32 @@ frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* 
   }
   CK(cudaStreamSynchronize(h->st));
   if (sweeps) CK(cudaMemcpy(sweeps, &h->dev->sweeps, sizeof(int), cudaMemcpyDeviceToHost));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                              const void* B, void* out) {
+  TRY(debug_pass_nosync(h, kind, impl, A, lda, B, out));
+  CK(cudaStreamSynchronize(h->st));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
+                                    const void* B, void* out, int32_t reps, double* ms) {
+  if (reps < 1 || !ms) return FRSVT_EINVAL;
+  TRY(debug_pass_nosync(h, kind, impl, A, lda, B, out));  // warm-up (and argument check)
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, h->st));
+  for (int i = 0; i < reps; ++i) TRY(debug_pass_nosync(h, kind, impl, A, lda, B, out));
+  CK(cudaEventRecord(e1, h->st));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, e0, e1));
+  *ms = t / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return FRSVT_OK;
 }
 

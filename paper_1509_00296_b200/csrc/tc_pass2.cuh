@@ -1,0 +1,665 @@
+// Persistent stream-K tcgen05 streaming pass over the m x n operand A (fp32
+// handles): the GEMM-shaped steps of Algorithm 1 (PAPER.md P:128 sketch,
+// P:141 power iteration, P:143/P:177 B = Q^T A).
+//   MODE_AX : Y (m x l) = A (m x n) X (n x l)      M = rows of A, K = n
+//   MODE_ATQ: Z (n x l) = A^T (n x m) Q (m x l)    M = columns of A, K = m
+//
+// Why this shape (measured on B200, profiles/r1_summary.md): A streams from
+// HBM once per pass, but the small operand B (X or Q) is re-read from L2 for
+// every 128-row tile. With B as fp32 hi + lo that is 2 bytes of L2 traffic
+// per byte of A, and the L2 slice throughput (~6300 B/cycle chip-wide, the
+// guide's LTS cap) was one bound of the old passes; here B is tf32 b_h (4 B)
+// + bf16 [b_l | b_h] (4 B) per element, re-read from L2 per tile.
+//
+// Products (fp32-level: 1xTF32 misses 1e-4):
+//   a b ~= a_h b_h + bf16(a_h) bf16(b_l) + bf16(a_l) bf16(b_h)
+// with a_h = rna_tf32(a), a_l = a - a_h, b_h = rna_tf32(b), b_l = b - b_h.
+// The dropped a_l b_l is ~2^-22 |ab|, the bf16 roundings of the two cross
+// terms ~2^-19 |ab| each; measured relative error of a pass ~1e-6
+// (tests/test_gpu_tc.py). The two cross terms are one bf16 product over a
+// doubled K: [bf16(a_h) | bf16(a_l)] . [bf16(b_l) ; bf16(b_h)]. Per 32-wide K
+// chunk: 4 tf32 MMAs (K = 8) + 4 bf16 MMAs (K = 16); measured on B200 (all
+// SMs busy, scripts/mma_rate.py) 70 and 81.5 cycles each, 606 tensor cycles
+// per 16 KB of A (3xTF32: 840). Under the 1 kW cap the SM clock settles near
+// 1.35 GHz during a pass, so tensor cycles, not HBM, bound these passes.
+//
+// Work: the M tiles x K chunks of the pass are flattened tile-major and cut
+// into gridDim.x contiguous ranges, one per CTA (stream-K): every SM streams
+// the same number of chunks, no wave tail. A range covering a whole tile
+// writes it directly; a tile split between CTAs leaves partial sums in a
+// per-CTA slot (first or last segment of the range) that tc_fixup_kernel adds
+// in CTA order (deterministic).
+//
+// Roles per CTA (640 threads):
+//   warp 0      TMA producer of A (16 KB chunks, 9-deep ring, released as soon as
+//               the converters hold the values in registers)
+//   warp 3      TMA producer of B_h (tf32, 128B swizzle) + B_l (bf16, 64B
+//               swizzle), 3-deep ring released by the MMA
+//   warp 1      MMA issuer (one thread); A operands from TMEM, B from smem
+//   warp 2      TMEM allocator
+//   warps 4..11 converters (two per TMEM lane quarter, 16 K values each):
+//               A chunk -> a_h, a_l (tf32) and bf16(a_h) pairs -> TMEM ring
+//               (thread = TMEM lane = M row)
+//   warps 12..19 flush: double-buffered TMEM accumulator pieces (<= SEG
+//               chunks, never across a tile) -> fp32 registers -> output
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "tc_pass.cuh"
+
+namespace frsvt {
+namespace tc {
+
+constexpr int P2_ASTAGES = 5;  // A ring (16 KB stages; released by the converters)
+constexpr int P2_BSTAGES = 4;  // B ring (32 KB stages; released by the MMA; L2 latency ~2400 cycles under load)
+constexpr int P2_TSTAGES = 4;  // TMEM A ring (64 columns per stage: a_h tf32 | bf16 a_h | bf16 a_l)
+constexpr int P2_SEG = 8;      // chunks accumulated in TMEM before a flush
+constexpr int P2_THREADS = 640;
+constexpr int P2_SLOTS = 2;    // partial-tile slots per CTA
+
+struct Pass2Smem {
+  static constexpr uint32_t a_bytes = 128u * BK * 4u;         // 16 KB
+  static constexpr uint32_t bh_bytes = 128u * BK * 4u;        // 16 KB (N <= 128 rows)
+  static constexpr uint32_t bx_bytes = 128u * 2 * BK * 2u;    // 16 KB: bf16 [b_l | b_h], 64 K per row
+  static constexpr uint32_t b_bytes = bh_bytes + bx_bytes;    // 32 KB
+  static constexpr size_t total() {
+    return 1024 + (size_t)P2_ASTAGES * a_bytes + (size_t)P2_BSTAGES * b_bytes + 512;
+  }
+};
+
+// Shared-memory descriptor: K-major, 64-byte swizzle (bf16 rows of 32 K), 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t desc_kmajor_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(512u >> 4) << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)4u << 61);
+}
+// Instruction descriptor: D fp32, A/B bf16 (kind::f16), both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void lds_u32x4(uint32_t saddr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(saddr) : "memory");
+}
+
+__device__ __forceinline__ uint64_t p2_gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// per-CTA global-timer stamps (dbg bit 6): [cta][0] entry, [1] producer done, [2] flush done, [3] exit
+__device__ __forceinline__ void p2_cta_stamp(int dbg, float* out, int ev) {
+  if (dbg & 64) reinterpret_cast<uint64_t*>(out)[40000 + blockIdx.x * 4 + ev] = p2_gtime();
+}
+__device__ __forceinline__ void p2_stamp(int dbg, float* out, int ev, int i, int nloc) {
+  if ((dbg & 32) && blockIdx.x == 0 && i < 4096) {
+    uint64_t* t = reinterpret_cast<uint64_t*>(out);
+    t[(int64_t)ev * 4096 + i] = clock64();
+  }
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(pred));
+  return pred != 0;
+}
+
+// Chunk range of CTA c: [c * total / G, (c + 1) * total / G).
+__host__ __device__ __forceinline__ int64_t p2_range_begin(int64_t total, int G, int c) {
+  return (total * c) / G;
+}
+
+// Walks the CTA's chunk range as a sequence of accumulator pieces: at most
+// P2_SEG chunks, never crossing a tile. All roles iterate it identically.
+struct P2Walk {
+  int64_t g, g1;   // next chunk, end of range
+  int nch;         // chunks per tile
+  __device__ __forceinline__ bool next(int& tile, int& k0, int& k1, bool& tile_first, bool& tile_last,
+                                       int64_t& seg_begin) {
+    if (g >= g1) return false;
+    tile = (int)(g / nch);
+    k0 = (int)(g - (int64_t)tile * nch);
+    const int64_t tile_end = (int64_t)(tile + 1) * nch;
+    const int64_t end = min(g1, tile_end);
+    tile_first = (g == seg_begin);
+    int kk = k0 + P2_SEG;
+    k1 = (int)min((int64_t)kk, end - (int64_t)tile * nch);
+    g = (int64_t)tile * nch + k1;
+    tile_last = (g == end);
+    if (tile_last) seg_begin = g;
+    return true;
+  }
+};
+
+template <int MODE, int NP>
+__global__ void __launch_bounds__(P2_THREADS, 1)
+tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
+                const __grid_constant__ CUtensorMap mapBl, int Mtot, int Ktot, int Nvalid, int nbrows,
+                float* __restrict__ out, int64_t ldo, const float* __restrict__ add, int64_t ldadd,
+                float* __restrict__ part, int dbg) {
+  // dbg (test hook only, 0 in production): bit 0 no MMA, bit 1 no conversion, bit 2 no B loads,
+  // bit 3 no bf16 MMAs, bit 4 no a_lo MMAs, bit 5 clock64 stamps of CTA 0 into out (output invalid)
+  static_assert(NP % 16 == 0 && NP >= 32 && NP <= 128, "N tile");
+  constexpr uint32_t A_BYTES = Pass2Smem::a_bytes;
+  constexpr uint32_t BH_BYTES = Pass2Smem::bh_bytes;
+  constexpr uint32_t B_BYTES = Pass2Smem::b_bytes;
+  constexpr int HALF = NP / 2;  // columns per flush warp
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;                                   // P2_ASTAGES x 16 KB
+  uint8_t* sB = smem + P2_ASTAGES * A_BYTES;            // P2_BSTAGES x 24 KB (Bh 16 KB | Bl 8 KB)
+  uint64_t* fulla = (uint64_t*)(sB + P2_BSTAGES * B_BYTES);
+  uint64_t* emptya = fulla + P2_ASTAGES;
+  uint64_t* fullb = emptya + P2_ASTAGES;
+  uint64_t* emptyb = fullb + P2_BSTAGES;
+  uint64_t* tfull = emptyb + P2_BSTAGES;
+  uint64_t* tempty = tfull + P2_TSTAGES;
+  uint64_t* accfull = tempty + P2_TSTAGES;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tslot = (uint32_t*)(accempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) p2_cta_stamp(dbg, out, 0);
+  const int nch = (Ktot + BK - 1) / BK;
+  const int mtiles = (Mtot + 127) / 128;
+  const int64_t total = (int64_t)mtiles * nch;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int64_t g0 = p2_range_begin(total, G, cta), g1 = p2_range_begin(total, G, cta + 1);
+  const int nloc = (int)(g1 - g0);
+  // expected TMA bytes per B stage (B boxes are nbrows rows)
+  const uint32_t btx = (uint32_t)nbrows * BK * 4u + (uint32_t)nbrows * 2 * BK * 2u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P2_ASTAGES; ++s) {
+      mbar_init(&fulla[s], 1);
+      mbar_init(&emptya[s], 8);
+    }
+    for (int s = 0; s < P2_BSTAGES; ++s) {
+      mbar_init(&fullb[s], 1);
+      mbar_init(&emptyb[s], 1);
+    }
+    for (int t = 0; t < P2_TSTAGES; ++t) {
+      mbar_init(&tfull[t], 8);
+      mbar_init(&tempty[t], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tslot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t t_acc0 = tbase;     // accumulator buffer b at columns [128 b, 128 b + NP)
+  const uint32_t t_a = tbase + 256;  // A ring: stage t at 256 + 64 t
+
+  if (warp == 0) {
+    // A producer (HBM stream, deep ring)
+    if (lane == 0 && nloc > 0) {
+      prefetch_tmap(&mapA);
+      for (int i = 0; i < nloc; ++i) {
+        const int64_t g = g0 + i;
+        const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
+        const int s = i % P2_ASTAGES;
+        const uint32_t ph = (i / P2_ASTAGES) & 1;
+        mbar_wait(&emptya[s], ph ^ 1);
+        p2_stamp(dbg, out, 0, i, nloc);
+        mbar_expect_tx(&fulla[s], A_BYTES);
+        if (MODE == MODE_AX)
+          tma_load_2d(sA + s * A_BYTES, &mapA, &fulla[s], tile * 128, kc);
+        else
+          tma_load_2d(sA + s * A_BYTES, &mapA, &fulla[s], kc, tile * 128);
+      }
+      p2_cta_stamp(dbg, out, 1);
+    }
+  } else if (warp == 3) {
+    // B producer (L2-resident small operand)
+    if (lane == 0 && nloc > 0) {
+      prefetch_tmap(&mapBh);
+      prefetch_tmap(&mapBl);
+      for (int i = 0; i < nloc; ++i) {
+        const int64_t g = g0 + i;
+        const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
+        const int s = i % P2_BSTAGES;
+        const uint32_t ph = (i / P2_BSTAGES) & 1;
+        mbar_wait(&emptyb[s], ph ^ 1);
+        p2_stamp(dbg, out, 6, i, nloc);
+        if (dbg & 4) {
+          mbar_arrive(&fullb[s]);
+          continue;
+        }
+        mbar_expect_tx(&fullb[s], btx);
+        tma_load_2d(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0);
+        tma_load_2d(sB + s * B_BYTES + BH_BYTES, &mapBl, &fullb[s], 2 * kc, 0);
+      }
+    }
+  } else if (warp == 1) {
+    // The whole warp walks the schedule (warp-uniform values stay in uniform
+    // registers); one elected lane issues the tcgen05 instructions.
+    if (nloc > 0) {
+      constexpr uint32_t id_tf = idesc_tf32(128, NP);
+      constexpr uint32_t id_bf = idesc_bf16(128, NP);
+      const bool leader = elect_one();
+      P2Walk wk{g0, g1, nch};
+      int64_t sb = g0;
+      int tile, k0, k1;
+      bool tf, tl;
+      int i = 0, piece = 0;
+      const uint32_t sB_u = smem_u32(sB);
+      while (wk.next(tile, k0, k1, tf, tl, sb)) {
+        const int b = piece & 1;
+        mbar_wait(&accempty[b], ((piece >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc = t_acc0 + 128 * b;
+        for (int kc = k0; kc < k1; ++kc, ++i) {
+          const int s = i % P2_BSTAGES;
+          const uint32_t ph = (i / P2_BSTAGES) & 1;
+          const int t = i % P2_TSTAGES;
+          const uint32_t tph = (i / P2_TSTAGES) & 1;
+          mbar_wait(&fullb[s], ph);
+          if (leader) p2_stamp(dbg, out, 7, i, nloc);
+          mbar_wait(&tfull[t], tph);
+          tc_fence_after();
+          if (leader) p2_stamp(dbg, out, 4, i, nloc);
+          if (dbg & 1) {
+            if (leader) {
+              mbar_arrive(&emptyb[s]);
+              mbar_arrive(&tempty[t]);
+            }
+            __syncwarp();
+            continue;
+          }
+          const uint32_t st = sB_u + (uint32_t)s * B_BYTES;
+          const uint64_t bh = desc_kmajor_sw128(st);
+          const uint64_t bx = desc_kmajor_sw128(st + BH_BYTES);
+          const uint32_t a_hi = t_a + t * 64, a_x = a_hi + 32;
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t koff = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along K
+              mma_tf32_ts(acc, a_hi + kk * 8, bh + koff, id_tf, (kc > k0 || kk > 0) ? 1u : 0u);
+            }
+            if (!(dbg & 8)) {
+#pragma unroll
+              for (int kk = 0; kk < 2 * BK / 16; ++kk) {
+                const uint64_t koff = (uint64_t)(kk * 32) >> 4;  // 16 bf16 = 32 bytes along K'
+                mma_bf16_ts(acc, a_x + kk * 8, bx + koff, id_bf, 1u);
+              }
+            }
+            tc_commit(&emptyb[s]);
+            tc_commit(&tempty[t]);
+            p2_stamp(dbg, out, 5, i, nloc);
+          }
+          __syncwarp();
+        }
+        if (leader) {
+          if (dbg & 1) mbar_arrive(&accfull[b]);
+          else tc_commit(&accfull[b]);
+        }
+        __syncwarp();
+        ++piece;
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // converters: A chunk in shared memory -> a_h, a_l, bf16(a_h) -> TMEM ring.
+    // Two warps per TMEM lane quarter, each converting 16 of the chunk's 32 K.
+    const int wq = warp & 3, kh = (warp - 4) >> 2;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    for (int i = 0; i < nloc; ++i) {
+      const int s = i % P2_ASTAGES;
+      const uint32_t ph = (i / P2_ASTAGES) & 1;
+      const int t = i % P2_TSTAGES;
+      const uint32_t tph = (i / P2_TSTAGES) & 1;
+      mbar_wait(&fulla[s], ph);
+      if (warp == 4 && lane == 0) p2_stamp(dbg, out, 1, i, nloc);
+      if (dbg & 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptya[s]);
+        mbar_wait(&tempty[t], tph ^ 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfull[t]);
+        continue;
+      }
+      const uint32_t a_s = smem_u32(sA + s * A_BYTES);
+      uint32_t hi[16], lo[16], hb[8], lb[8];
+      if (MODE == MODE_AX) {
+        // box {128 rows, 32 cols}, no swizzle: (row, k) at (k*128 + row)*4
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hi[k] = lds_u32(a_s + (uint32_t)(((16 * kh + k) * 128 + row) * 4));
+      } else {
+        // box {32 rows (K), 128 cols (M)}, 128B swizzle: (j, k) at j*128 + ((k/4 ^ j%8) * 16) + (k%4)*4
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cc = 4 * kh + c;
+          lds_u32x4(a_s + (uint32_t)(row * 128 + ((cc ^ (row & 7)) * 16)), hi[4 * c], hi[4 * c + 1], hi[4 * c + 2],
+                    hi[4 * c + 3]);
+        }
+      }
+      // the A stage is free once its values are in registers
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptya[s]);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t x = hi[k];
+        const uint32_t h = (x + 0x1000u) & 0xFFFFE000u;  // round to nearest tf32, ties away (finite x)
+        hi[k] = h;
+        lo[k] = __float_as_uint(__uint_as_float(x) - __uint_as_float(h));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const __nv_bfloat162 p = __floats2bfloat162_rn(__uint_as_float(hi[2 * k]), __uint_as_float(hi[2 * k + 1]));
+        hb[k] = *reinterpret_cast<const uint32_t*>(&p);
+        const __nv_bfloat162 q = __floats2bfloat162_rn(__uint_as_float(lo[2 * k]), __uint_as_float(lo[2 * k + 1]));
+        lb[k] = *reinterpret_cast<const uint32_t*>(&q);
+      }
+      mbar_wait(&tempty[t], tph ^ 1);
+      if (warp == 4 && lane == 0) p2_stamp(dbg, out, 2, i, nloc);
+      // stage layout: [0, 32) a_h tf32; [32, 48) bf16 a_h pairs (K' 0..31); [48, 64) bf16 a_l pairs (K' 32..63)
+      const uint32_t ta = t_a + t * 64 + lane_off;
+      tmem_st16(ta + 16 * kh, hi);
+      tmem_st8(ta + 32 + 8 * kh, hb);
+      tmem_st8(ta + 48 + 8 * kh, lb);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[t]);
+      if (warp == 4 && lane == 0) p2_stamp(dbg, out, 3, i, nloc);
+    }
+  } else if (warp >= 12) {
+    // flush warps: accumulator pieces -> fp32 registers -> output / partial slot
+    const int wq = warp & 3;
+    const int col0 = ((warp - 12) >> 2) * HALF;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    float sum[HALF];
+#pragma unroll
+    for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
+    P2Walk wk{g0, g1, nch};
+    int64_t sb = g0;
+    int tile, k0, k1;
+    bool tf, tl;
+    int piece = 0, seg = 0;
+    int tile_k0 = 0;
+    while (wk.next(tile, k0, k1, tf, tl, sb)) {
+      if (tf) tile_k0 = k0;
+      const int b = piece & 1;
+      mbar_wait(&accfull[b], (piece >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < HALF; cb += 16) {
+        uint32_t v[16];
+        tmem_ld16(t_acc0 + 128 * b + col0 + cb + lane_off, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum[cb + j] += __uint_as_float(v[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[b]);
+      ++piece;
+      if (tl && !(dbg & 96)) {
+        const bool whole = (tile_k0 == 0) && (k1 == nch);
+        const int gm = tile * 128 + row;
+        if (whole) {
+          if (gm < Mtot) {
+#pragma unroll
+            for (int j = 0; j < HALF; ++j) {
+              const int c = col0 + j;
+              if (c < Nvalid) {
+                float x = sum[j];
+                if (add) x += add[gm + (int64_t)c * ldadd];
+                out[gm + (int64_t)c * ldo] = x;
+              }
+            }
+          }
+        } else {
+          // slot 0: the range's first (partial) segment, slot 1: its last
+          const int slot = (seg == 0) ? 0 : 1;
+          float* p = part + ((int64_t)cta * P2_SLOTS + slot) * 128 * NP;
+#pragma unroll
+          for (int j = 0; j < HALF; ++j) p[(int64_t)(col0 + j) * 128 + row] = sum[j];
+        }
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
+        ++seg;
+      }
+    }
+  }
+  if (warp == 12 && lane == 0) p2_cta_stamp(dbg, out, 2);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+  if (threadIdx.x == 0) p2_cta_stamp(dbg, out, 3);
+}
+
+// Tiles split between CTAs: out = sum of the covering CTAs' partial slots (in
+// CTA order) (+ add). One block per tile; the covering CTAs and their slots
+// are resolved once per block (gridDim of the pass G <= 256).
+template <int NP>
+__global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
+                                                       const float* __restrict__ part, float* __restrict__ out,
+                                                       int64_t ldo, const float* __restrict__ add, int64_t ldadd) {
+  __shared__ int64_t soff[256];
+  __shared__ int ncov;
+  const int nch = (Ktot + BK - 1) / BK;
+  const int mtiles = (Mtot + 127) / 128;
+  const int64_t total = (int64_t)mtiles * nch;
+  const int tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+    const int64_t t0 = (int64_t)tile * nch, t1 = t0 + nch;
+    // CTAs whose range intersects [t0, t1)
+    int c0 = (int)((t0 * G) / total);
+    while (c0 > 0 && p2_range_begin(total, G, c0) > t0) --c0;
+    while (p2_range_begin(total, G, c0 + 1) <= t0) ++c0;
+    int c1 = c0;
+    while (c1 + 1 < G && p2_range_begin(total, G, c1 + 1) < t1) ++c1;
+    const bool whole = (c0 == c1) && p2_range_begin(total, G, c0) <= t0 && p2_range_begin(total, G, c0 + 1) >= t1;
+    int k = 0;
+    if (!whole) {
+      for (int cc = c0; cc <= c1 && k < 256; ++cc) {
+        const int64_t b = p2_range_begin(total, G, cc);
+        if (p2_range_begin(total, G, cc + 1) <= b) continue;  // empty range
+        const int slot = (b >= t0) ? 0 : 1;                      // tile holds the range's first / last segment
+        soff[k++] = ((int64_t)cc * P2_SLOTS + slot) * 128 * NP;
+      }
+    }
+    ncov = k;
+  }
+  __syncthreads();
+  const int nc = ncov;
+  if (nc == 0) return;  // written directly by the pass
+  for (int idx = threadIdx.x; idx < 128 * Nvalid; idx += blockDim.x) {
+    const int row = idx & 127, c = idx >> 7;
+    const int gm = tile * 128 + row;
+    if (gm >= Mtot) continue;
+    float acc = 0.f;
+    for (int k = 0; k < nc; ++k) acc += part[soff[k] + (int64_t)c * 128 + row];
+    if (add) acc += add[gm + (int64_t)c * ldadd];
+    out[gm + (int64_t)c * ldo] = acc;
+  }
+}
+
+// B operand split: Bh = rna_tf32(x) (fp32, rows x cols, ld ldh) and Bx (bf16,
+// (2 * roundup32(rows)) x cols, ld ldx): for K chunk c, Bx rows 64c + j hold
+// bf16(x - Bh) at K = 32c + j (j < 32) and bf16(Bh) at K = 32c + j - 32
+// (j >= 32), zero past `rows`. One thread per Bx element.
+__global__ void split_tf32_bf16x2_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx_in,
+                                         float* __restrict__ Bh, int64_t ldh, __nv_bfloat16* __restrict__ Bx,
+                                         int64_t ldx) {
+  const int64_t kp = ((rows + 31) / 32) * 64;
+  const int64_t total = kp * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r2 = idx % kp, j = idx / kp;
+    const int64_t c = r2 >> 6, w = r2 & 63;
+    const int64_t k = 32 * c + (w & 31);
+    float v = 0.f;
+    if (k < rows) {
+      const float x = X[k + j * ldx_in];
+      const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+      if (w < 32) {
+        v = x - h;
+        Bh[k + j * ldh] = h;
+      } else {
+        v = h;
+      }
+    }
+    Bx[r2 + j * ldx] = __float2bfloat16_rn(v);
+  }
+}
+
+}  // namespace tc
+}  // namespace frsvt
+
+namespace frsvt {
+namespace tc {
+// Bandwidth probe (test hook only): streams the A operand of a pass through
+// the same persistent stream-K partition and TMA ring as tc_pass2_kernel, with
+// no math (one consumer warp releases each stage as soon as it lands).
+// Separates the DRAM/TMA streaming rate from the MMA/converter pipeline.
+template <int MODE, int SUB>
+__global__ void __launch_bounds__(64, 1)
+tma_stream_probe_kernel(const __grid_constant__ CUtensorMap mapA, int Mtot, int Ktot, float* __restrict__ sink) {
+  constexpr int ST = 8 / SUB;
+  constexpr uint32_t SUB_BYTES = 128u * BK * 4u;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + ST * SUB * SUB_BYTES);
+  uint64_t* empty = full + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = (Ktot + BK * SUB - 1) / (BK * SUB);
+  const int mtiles = (Mtot + 127) / 128;
+  const int64_t total = (int64_t)mtiles * nch;
+  const int64_t g0 = p2_range_begin(total, gridDim.x, blockIdx.x), g1 = p2_range_begin(total, gridDim.x, blockIdx.x + 1);
+  const int nloc = (int)(g1 - g0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < nloc; ++i) {
+      const int64_t g = g0 + i;
+      const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK * SUB;
+      const int s = i % ST;
+      mbar_wait(&empty[s], ((i / ST) & 1) ^ 1);
+      mbar_expect_tx(&full[s], SUB * SUB_BYTES);
+      for (int u = 0; u < SUB; ++u) {
+        uint8_t* dst = smem + (s * SUB + u) * SUB_BYTES;
+        if (MODE == MODE_AX)
+          tma_load_2d(dst, &mapA, &full[s], tile * 128, kc + u * BK);
+        else
+          tma_load_2d(dst, &mapA, &full[s], kc + u * BK, tile * 128);
+      }
+    }
+  } else if (warp == 1) {
+    float acc = 0.f;
+    for (int i = 0; i < nloc; ++i) {
+      const int s = i % ST;
+      mbar_wait(&full[s], (i / ST) & 1);
+      acc += ((const float*)(smem + s * SUB * SUB_BYTES))[lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (acc == 1234.5f) sink[blockIdx.x] = acc;
+  }
+}
+}  // namespace tc
+}  // namespace frsvt
+
+namespace frsvt {
+namespace tc {
+// Tensor-pipe rate probe (test hook only): one CTA per SM issues `reps`
+// groups of MMAs back to back into one TMEM accumulator (M = 128, N = 128),
+// A from TMEM, B from (uninitialised) shared memory; writes cycles per MMA of
+// CTA 0 to out[0]. kind 0: tf32 (K = 8), 1: bf16 (K = 16), 2: tf32 with the
+// A operand from shared memory (SS), 3: tf32 N = 256.
+__global__ void __launch_bounds__(128, 1) mma_rate_probe_kernel(int kind, int reps, float* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(&tslot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tslot;
+  if (warp == 1) {
+    const bool leader = elect_one();
+    const uint32_t sb = smem_u32(smem);
+    const uint64_t bd = desc_kmajor_sw128(sb), ad = desc_kmajor_sw128(sb + 32768);
+    const uint32_t it = idesc_tf32(128, kind == 3 ? 256 : 128), ib = idesc_bf16(128, 128);
+    long long t0 = clock64();
+    if (leader) {
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ko = (uint64_t)(kk * 32) >> 4;
+          if (kind == 0 || kind == 3) mma_tf32_ts(tb, tb + 256 + kk * 8, bd + ko, it, 1u);
+          else if (kind == 1) mma_bf16_ts(tb, tb + 256 + kk * 8, bd + ko, ib, 1u);
+          else mma_tf32_ss(tb, ad + ko, bd + ko, it, 1u);
+        }
+      }
+      tc_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (leader && blockIdx.x == 0) out[0] = (float)(t1 - t0) / (float)(reps * 4);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tb, 512);
+  }
+}
+}  // namespace tc
+}  // namespace frsvt
