@@ -340,7 +340,8 @@ frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q
 // ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
 template <int MODE, int NP>
 frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
-                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0) {
+                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
+                          const int* rp_dev = nullptr) {
   const size_t smem = tc::Pass2Smem::total();
   static bool attr_set = false;
   if (!attr_set) {
@@ -351,10 +352,10 @@ frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
   const int64_t total = (int64_t)mtiles * cdiv(Ktot, tc::BK);
   const int G = (int)(total < h->nsm ? total : h->nsm);
   tc::tc_pass2_kernel<MODE, NP><<<G, tc::P2_THREADS, smem, h->st>>>(mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo,
-                                                                    add, ldadd, h->skpart, dbg);
+                                                                    add, ldadd, h->skpart, rp_dev, dbg);
   TRY(post_launch(h));
   if (dbg & 96) return FRSVT_OK;
-  tc::tc_fixup_kernel<NP><<<mtiles, 256, 0, h->st>>>(Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd);
+  tc::tc_fixup_kernel<NP><<<mtiles, 256, 0, h->st>>>(Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
   return post_launch(h);
 }
 
@@ -362,7 +363,8 @@ frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
 // MODE_AX: A is Mtot x Ktot (lda); MODE_ATQ: A is Ktot x Mtot (lda), op = ^T.
 template <int MODE>
 frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
-                      int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0) {
+                      int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
+                      const int* rp_dev = nullptr) {
   float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
   __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
   const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
@@ -385,9 +387,11 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   }
   if (!ok) return FRSVT_ECUDA;
   const int np = tc_np(h->l);
-  if (np == 32) return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
-  if (np == 64) return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
-  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg);
+  if (np == 32)
+    return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+  if (np == 64)
+    return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
 }
 
 // tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows) matrix
@@ -590,11 +594,24 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
                           bool use_carry, int64_t call) {
   const int l = h->l;
   const T* ov = h->override_pending ? (const T*)h->OmOv : nullptr;
+  // RP on the stream-K path: multiply only the p fresh columns (Alg. 1 RP
+  // branch) and place them behind the carried Q~
+  bool rp_front = false;
+  if constexpr (sizeof(T) == 4) rp_front = use_carry && h->pass2 && tc_eligible(h, A, lda);
   omega_kernel<T><<<grid1d(h->n * l), 256, 0, h->st>>>((T*)h->Om, h->n, l, &h->dev->r, use_carry ? 1 : 0,
-                                                       h->cfg.seed, stream + (uint32_t)call, ov, h->n);
+                                                       h->cfg.seed, stream + (uint32_t)call, ov, h->n,
+                                                       rp_front ? 1 : 0);
   TRY(post_launch(h));
   h->override_pending = 0;
-  TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
+  if constexpr (sizeof(T) == 4) {
+    if (rp_front) {
+      TRY(prof_begin(h));
+      TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y, h->m,
+                                (const float*)h->Qt, h->m, 0, &h->dev->r));
+      TRY(prof_end(h, 0, (double)h->m * h->n * sizeof(T)));
+    }
+  }
+  if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
   const bool sh = h->cfg.nranks > 1;
   TRY(orth<T>(h, (const T*)h->Y, h->m, (T*)h->Q, (T*)h->Qtmp, sh));
   for (int it = 0; it < q; ++it) {
@@ -1131,7 +1148,7 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : 
 
 static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                                       const void* B, void* out) {
-  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 143) return FRSVT_EINVAL;
+  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 144) return FRSVT_EINVAL;
   if (impl >= 8 && impl <= 135 && h->esz == 4 && tma_encode_available()) {  // pass2 with pipeline parts disabled
     frsvt_status st = kind == 0 ? tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n,
                                                        (float*)out, h->m, nullptr, 0, impl - 8)
@@ -1139,7 +1156,7 @@ static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t imp
                                                         (float*)out, h->n, nullptr, 0, impl - 8);
     return st;
   }
-  if (impl >= 140 && impl <= 143 && h->esz == 4) {  // tensor-pipe rate probe, out[0] = cycles per MMA
+  if (impl >= 140 && impl <= 144 && h->esz == 4) {  // tensor-pipe rate probe, out[0] = cycles per MMA
     static bool attr = false;
     if (!attr) {
       CK(cudaFuncSetAttribute(tc::mma_rate_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));

@@ -39,11 +39,13 @@ __device__ __forceinline__ double philox_normal(uint64_t seed, uint32_t stream, 
 
 // Omega' (n x l, ld n): columns [r, r+p) hold columns [0, p) of Omega of this
 // call (p = l - r, RP reading Z6), columns < r are zero so that
-// A * Omega' + Q~ = [Q~ | A Omega_p]. r = 0 without a carry.
+// A * Omega' + Q~ = [Q~ | A Omega_p]. r = 0 without a carry. With front != 0
+// the p fresh columns sit at [0, p) instead (the stream-K sketch multiplies
+// only them and writes them behind the carried columns).
 template <typename T>
 __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __restrict__ r_dev,
                              int use_r, uint64_t seed, uint32_t stream,
-                             const T* __restrict__ override_om, int64_t ldo) {
+                             const T* __restrict__ override_om, int64_t ldo, int front = 0) {
   const int r = use_r ? *r_dev : 0;
   const int64_t total = n * (int64_t)l;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -51,8 +53,8 @@ __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __
     const int64_t i = idx % n;
     const int c = (int)(idx / n);
     T v = T(0);
-    if (c >= r) {
-      const int src = c - r;
+    if (front ? (c < l - r) : (c >= r)) {
+      const int src = front ? c : c - r;
       if (override_om) v = override_om[i + src * ldo];
       else v = (T)philox_normal(seed, stream, (uint64_t)src * (uint64_t)n + (uint64_t)i);
     }

@@ -162,7 +162,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
 tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
                 const __grid_constant__ CUtensorMap mapBl, int Mtot, int Ktot, int Nvalid, int nbrows,
                 float* __restrict__ out, int64_t ldo, const float* __restrict__ add, int64_t ldadd,
-                float* __restrict__ part, int dbg) {
+                float* __restrict__ part, const int* __restrict__ rp_dev, int dbg) {
+  // rp_dev (MODE_AX, range propagation): r = *rp_dev carried columns; only the
+  // p = Nvalid - r fresh columns are multiplied (B holds them at [0, p), the
+  // MMA runs with N = roundup16(p)) and land in out[:, r + c]; out[:, :r] is a
+  // copy of add[:, :r] (the carry Q~).
   // dbg (test hook only, 0 in production): bit 0 no MMA, bit 1 no conversion, bit 2 no B loads,
   // bit 3 no bf16 MMAs, bit 4 no a_lo MMAs, bit 5 clock64 stamps of CTA 0 into out (output invalid)
   static_assert(NP % 16 == 0 && NP >= 32 && NP <= 128, "N tile");
@@ -179,13 +183,21 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   uint64_t* fullb = emptya + P2_ASTAGES;
   uint64_t* emptyb = fullb + P2_BSTAGES;
   uint64_t* tfull = emptyb + P2_BSTAGES;
-  uint64_t* tempty = tfull + P2_TSTAGES;
-  uint64_t* accfull = tempty + P2_TSTAGES;
+  // one MMA-completion barrier per stage frees both the B stage and the TMEM
+  // A stage of a chunk (one tcgen05.commit per chunk)
+  static_assert(P2_BSTAGES == P2_TSTAGES, "B and TMEM rings share the completion barrier");
+  uint64_t* tempty = emptyb;
+  uint64_t* accfull = tfull + P2_TSTAGES;
   uint64_t* accempty = accfull + 2;
   uint32_t* tslot = (uint32_t*)(accempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) p2_cta_stamp(dbg, out, 0);
+  const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;   // output column shift
+  const int nact = Nvalid - rsh;                               // multiplied columns
+  // MMA N: the valid columns rounded up to 8 (N steps of 8 are legal at
+  // cta_group::1; measured 60 cycles at N = 120 vs 64 at 128)
+  const int nmma = min(NP, max(16, ((rp_dev ? nact : Nvalid) + 7) & ~7));
   const int nch = (Ktot + BK - 1) / BK;
   const int mtiles = (Mtot + 127) / 128;
   const int64_t total = (int64_t)mtiles * nch;
@@ -204,10 +216,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       mbar_init(&fullb[s], 1);
       mbar_init(&emptyb[s], 1);
     }
-    for (int t = 0; t < P2_TSTAGES; ++t) {
-      mbar_init(&tfull[t], 8);
-      mbar_init(&tempty[t], 1);
-    }
+    for (int t = 0; t < P2_TSTAGES; ++t) mbar_init(&tfull[t], 8);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], 8);
@@ -269,8 +278,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     // The whole warp walks the schedule (warp-uniform values stay in uniform
     // registers); one elected lane issues the tcgen05 instructions.
     if (nloc > 0) {
-      constexpr uint32_t id_tf = idesc_tf32(128, NP);
-      constexpr uint32_t id_bf = idesc_bf16(128, NP);
+      const uint32_t id_tf = idesc_tf32(128, nmma);
+      const uint32_t id_bf = idesc_bf16(128, nmma);
       const bool leader = elect_one();
       P2Walk wk{g0, g1, nch};
       int64_t sb = g0;
@@ -296,7 +305,6 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           if (dbg & 1) {
             if (leader) {
               mbar_arrive(&emptyb[s]);
-              mbar_arrive(&tempty[t]);
             }
             __syncwarp();
             continue;
@@ -319,7 +327,6 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
               }
             }
             tc_commit(&emptyb[s]);
-            tc_commit(&tempty[t]);
             p2_stamp(dbg, out, 5, i, nloc);
           }
           __syncwarp();
@@ -438,7 +445,10 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < HALF; ++j) {
               const int c = col0 + j;
-              if (c < Nvalid) {
+              if (rp_dev) {
+                if (c < nact) out[gm + (int64_t)(rsh + c) * ldo] = sum[j];
+                if (c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+              } else if (c < Nvalid) {
                 float x = sum[j];
                 if (add) x += add[gm + (int64_t)c * ldadd];
                 out[gm + (int64_t)c * ldo] = x;
@@ -474,7 +484,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 template <int NP>
 __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
                                                        const float* __restrict__ part, float* __restrict__ out,
-                                                       int64_t ldo, const float* __restrict__ add, int64_t ldadd) {
+                                                       int64_t ldo, const float* __restrict__ add, int64_t ldadd,
+                                                       const int* __restrict__ rp_dev) {
   __shared__ int64_t soff[256];
   __shared__ int ncov;
   const int nch = (Ktot + BK - 1) / BK;
@@ -504,13 +515,19 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
   __syncthreads();
   const int nc = ncov;
   if (nc == 0) return;  // written directly by the pass
+  const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
   for (int idx = threadIdx.x; idx < 128 * Nvalid; idx += blockDim.x) {
     const int row = idx & 127, c = idx >> 7;
     const int gm = tile * 128 + row;
     if (gm >= Mtot) continue;
+    if (rp_dev && c < rsh) {  // carried column
+      out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+      continue;
+    }
+    const int ca = c - rsh;  // accumulator column
     float acc = 0.f;
-    for (int k = 0; k < nc; ++k) acc += part[soff[k] + (int64_t)c * 128 + row];
-    if (add) acc += add[gm + (int64_t)c * ldadd];
+    for (int k = 0; k < nc; ++k) acc += part[soff[k] + (int64_t)ca * 128 + row];
+    if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
     out[gm + (int64_t)c * ldo] = acc;
   }
 }
@@ -612,7 +629,7 @@ namespace tc {
 // groups of MMAs back to back into one TMEM accumulator (M = 128, N = 128),
 // A from TMEM, B from (uninitialised) shared memory; writes cycles per MMA of
 // CTA 0 to out[0]. kind 0: tf32 (K = 8), 1: bf16 (K = 16), 2: tf32 with the
-// A operand from shared memory (SS), 3: tf32 N = 256.
+// A operand from shared memory (SS), 3: tf32 N = 256, 4: tf32 N = 120.
 __global__ void __launch_bounds__(128, 1) mma_rate_probe_kernel(int kind, int reps, float* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -635,14 +652,14 @@ __global__ void __launch_bounds__(128, 1) mma_rate_probe_kernel(int kind, int re
     const bool leader = elect_one();
     const uint32_t sb = smem_u32(smem);
     const uint64_t bd = desc_kmajor_sw128(sb), ad = desc_kmajor_sw128(sb + 32768);
-    const uint32_t it = idesc_tf32(128, kind == 3 ? 256 : 128), ib = idesc_bf16(128, 128);
+    const uint32_t it = idesc_tf32(128, kind == 3 ? 256 : (kind == 4 ? 120 : 128)), ib = idesc_bf16(128, 128);
     long long t0 = clock64();
     if (leader) {
       for (int r = 0; r < reps; ++r) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint64_t ko = (uint64_t)(kk * 32) >> 4;
-          if (kind == 0 || kind == 3) mma_tf32_ts(tb, tb + 256 + kk * 8, bd + ko, it, 1u);
+          if (kind == 0 || kind >= 3) mma_tf32_ts(tb, tb + 256 + kk * 8, bd + ko, it, 1u);
           else if (kind == 1) mma_bf16_ts(tb, tb + 256 + kk * 8, bd + ko, ib, 1u);
           else mma_tf32_ss(tb, ad + ko, bd + ko, it, 1u);
         }

@@ -11,7 +11,7 @@ m, n, l = 4096, 4096, 120
 A = torch.zeros((n, m), device="cuda").t()
 B = torch.zeros((l, n), device="cuda").t()
 h = P.Frsvt(m, n, l, 1, dtype=torch.float32, seed=1)
-for kind, name in enumerate(["tf32 TS N128", "bf16 TS N128", "tf32 SS N128", "tf32 TS N256"]):
+for kind, name in enumerate(["tf32 TS N128", "bf16 TS N128", "tf32 SS N128", "tf32 TS N256", "tf32 TS N120"]):
     out = h.debug_pass(0, 140 + kind, A, B)
     out = h.debug_pass(0, 140 + kind, A, B)
     ms = h.debug_pass_timed(0, 140 + kind, A, B, 5)
