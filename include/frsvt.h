@@ -195,6 +195,13 @@ frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl,
 frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* G, double* Gcopy, double* sigma,
                                    double* UB, int32_t* sweeps, int32_t reps, double* ms);
 
+/* Test hook: the CholeskyQR factor kernel alone on an l x l fp64 Gram G
+ * (device, column-major): T (device, l x l, handle dtype) with Y T an
+ * orthonormal basis of range(Y) for Y^T Y = G, *s (host, nullable) = kept
+ * rank; stamps (device, nullable, >= 8 x u64) = %globaltimer at phase
+ * boundaries. Synchronises. */
+frsvt_status frsvt_debug_chol(frsvt_handle* h, const double* G, void* T, int32_t* s, unsigned long long* stamps);
+
 /* Pass profiling: with enable != 0 every kernel that streams the m x n
  * operand is bracketed by CUDA events on the handle's stream (enabling resets
  * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,

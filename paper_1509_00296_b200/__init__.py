@@ -265,6 +265,19 @@ class Frsvt:
             ctypes.c_void_p(out.data_ptr()), int(reps), ctypes.byref(ms)))
         return ms.value
 
+    def debug_chol(self, G, stamps=False):
+        """CholeskyQR factor T of an l x l Gram; returns (T, s[, stamps ns])."""
+        l = self.l
+        dev = torch.device("cuda", torch.cuda.current_device())
+        G = G.to(device=dev, dtype=torch.float64).t().contiguous().t()
+        T = torch.empty((l, l), dtype=self.dtype, device=dev).t()
+        st = torch.zeros(8, dtype=torch.int64, device=dev) if stamps else None
+        s = ctypes.c_int32()
+        _check("frsvt_debug_chol", lib.frsvt_debug_chol(self._h, ctypes.c_void_p(G.data_ptr()),
+                                                        ctypes.c_void_p(T.data_ptr()), ctypes.byref(s),
+                                                        ctypes.c_void_p(st.data_ptr() if st is not None else 0)))
+        return (T, s.value, st.cpu().numpy()) if stamps else (T, s.value)
+
     def profile(self, enable=True):
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 

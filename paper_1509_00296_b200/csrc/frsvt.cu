@@ -17,6 +17,7 @@
 #include "small2.cuh"
 #include "eig_jacobi.cuh"
 #include "orth_chol.cuh"
+#include "lowdin.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
 #include "tc_pass2.cuh"
@@ -69,6 +70,11 @@ struct frsvt_handle {
   int64_t ldxs, ldqs;
   int use_tc;
   int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
+  int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
+  double* E2b;       // Loewdin workspace E^2 (l x l fp64)
+  double *T2d, *Hd, *McD, *MpD;  // fp64 l x l: pending second CholeskyQR factor and fold scratch
+  int t2_pending;    // 1: h->Q holds Q1 and the basis is Q1 T2d (T2d folded into G, Mc, Mp)
+  int* lwd;          // device ints: [0] ok flag, [2..3] max|E| (u64)
   int nsm;           // SMs of the device (stream-K grid)
   float* skpart;     // stream-K partial-tile slots (nsm x 2 x 128 x 128 fp32)
   __nv_bfloat16 *Xb, *Qb;  // bf16 [b_l | b_h] operands of the stream-K passes (ld ldb16)
@@ -355,7 +361,9 @@ frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
                                                                     add, ldadd, h->skpart, rp_dev, dbg);
   TRY(post_launch(h));
   if (dbg & 96) return FRSVT_OK;
-  tc::tc_fixup_kernel<NP><<<mtiles, 256, 0, h->st>>>(Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
+  // one block per (tile, 8-column group): enough independent loads in flight
+  tc::tc_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
+      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
   return post_launch(h);
 }
 
@@ -469,12 +477,29 @@ frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sh
 }
 
 template <typename T>
-frsvt_status chol(frsvt_handle* h, T* Tout) {
+frsvt_status chol(frsvt_handle* h, T* Tout, const int* skip = nullptr) {
   const int l = h->l;
   const double tol = sizeof(T) == 4 ? 1e-12 : 1e-13;
   orth_chol_kernel<T><<<1, OC_THREADS, orth_chol_smem_bytes(l), h->st>>>(h->G, l, tol, Tout, &h->dev->s,
-                                                                          &h->dev->flags);
+                                                                          &h->dev->flags, nullptr, skip);
   return post_launch(h);
+}
+
+// second-pass factor T2 of the nearly orthonormal Q1 (Gram in h->G): the
+// Loewdin series when max|G - I| <= 0.05, else the Cholesky kernel (lowdin.cuh)
+template <typename T>
+frsvt_status chol2(frsvt_handle* h, T* Tout) {
+  if (!h->lowdin) return chol<T>(h, Tout);
+  const int l = h->l;
+  int* ok = h->lwd;
+  unsigned long long* emax = (unsigned long long*)(h->lwd + 2);
+  CK(cudaMemsetAsync(emax, 0, sizeof(unsigned long long), h->st));
+  const dim3 g((unsigned)cdiv(l, 32), (unsigned)cdiv(l, 32));
+  lowdin_sq_kernel<<<g, LWD_THREADS, lowdin_smem_bytes(l), h->st>>>(h->G, l, h->E2b, emax);
+  TRY(post_launch(h));
+  lowdin_series_kernel<T><<<g, LWD_THREADS, lowdin_smem_bytes(l), h->st>>>(h->G, h->E2b, l, emax, ok, Tout);
+  TRY(post_launch(h));
+  return chol<T>(h, Tout, ok);
 }
 
 // Out (rows x l) = In (rows x l) * M (l x l), fp32-accurate SIMT (used where
@@ -518,16 +543,38 @@ frsvt_status gram_fast(frsvt_handle* h, const T* Y, int64_t rows, bool sharded) 
   return gram<T>(h, Y, rows, rows, sharded);
 }
 
-// CholeskyQR2 with pivoted truncated Cholesky (readings R2/R4 in DESIGN.md):
-// pass 1 fp64 Gram + fp32-accurate apply, pass 2 on the nearly orthonormal Q1
+// C (l x l) = op(A) op(B) in fp64 (small multi-CTA product)
+template <typename Tout>
+frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, int tb, Tout* C) {
+  const int l = h->l;
+  const dim3 g((unsigned)cdiv(l, 32), (unsigned)cdiv(l, 32));
+  sgemm64_kernel<Tout><<<g, LWD_THREADS, (size_t)64 * l * sizeof(double), h->st>>>(l, l, l, A, l, ta, B, l, tb, C, l);
+  return post_launch(h);
+}
+
+// CholeskyQR, first pass (readings R2/R4 in DESIGN.md): fp64 Gram, Cholesky
+// with column drop, fp32-accurate apply. Out = Y T1 spans range(Y) and is
+// orthonormal up to ~u kappa(Y): enough wherever only the span of the basis
+// matters next (the next orthonormalisation follows: the sketch before a
+// power step, Z = A^T Q before A Z), so the second pass runs only on the
+// final basis of the range finder (orth_final).
 template <typename T>
-frsvt_status orth(frsvt_handle* h, const T* In, int64_t rows, T* Out, T* Tmp, bool sharded) {
+frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
   TRY(gram<T>(h, In, rows, rows, sharded));
   TRY(chol<T>(h, (T*)h->T1));
-  TRY(apply_small<T>(h, In, rows, rows, (const T*)h->T1, Tmp, rows));
-  TRY(gram_fast<T>(h, Tmp, rows, sharded));
-  TRY(chol<T>(h, (T*)h->T1));
-  TRY(apply_fast<T>(h, Tmp, rows, (const T*)h->T1, Out));
+  return apply_small<T>(h, In, rows, rows, (const T*)h->T1, Out, rows);
+}
+
+// Final basis of the range finder: CholeskyQR2 = orth1 + a second factor T2 of
+// the computed Q1 (Loewdin series or Cholesky, fp64). Q1 T2 is never formed:
+// T2 is folded into the l x l factors downstream (t2_pending; small_svd,
+// shrink_and_factors): B^T = (A^T Q1) T2, Q~ = Q1 (T2 Mc), Wt = (A^T Q1) (T2 Mp).
+template <typename T>
+frsvt_status orth_final(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
+  TRY(orth1<T>(h, In, rows, Out, sharded));
+  TRY(gram_fast<T>(h, Out, rows, sharded));
+  TRY(chol2<double>(h, h->T2d));
+  h->t2_pending = 1;
   return FRSVT_OK;
 }
 
@@ -613,12 +660,15 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   }
   if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
   const bool sh = h->cfg.nranks > 1;
-  TRY(orth<T>(h, (const T*)h->Y, h->m, (T*)h->Q, (T*)h->Qtmp, sh));
+  h->t2_pending = 0;
+  if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh);
+  TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
   for (int it = 0; it < q; ++it) {
     TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
-    TRY(orth<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, (T*)h->Zt, false));
+    TRY(orth1<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, false));
     TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr));
-    TRY(orth<T>(h, (const T*)h->Y, h->m, (T*)h->Q, (T*)h->Qtmp, sh));
+    if (it + 1 < q) TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
+    else TRY(orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
   }
   return FRSVT_OK;
 }
@@ -667,6 +717,10 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
                        const double* t_dev = nullptr) {
   TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
   TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
+  if (h->t2_pending) {  // G = T2^T (Z'^T Z') T2 for B^T = Z' T2
+    TRY(gemm_ll<double>(h, h->G, 0, h->T2d, 0, h->Hd));
+    TRY(gemm_ll<double>(h, h->T2d, 1, h->Hd, 0, h->G));
+  }
   return launch_eig(h, 0, h->G, h->sigma, h->UB, t_mode, t_host, t_dev);
 }
 
@@ -675,10 +729,19 @@ template <typename T>
 frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const double* tau_dev,
                                 double C, double eps) {
   const int l = h->l;
-  shrink_kernel<T><<<1, 128, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec,
-                                         C, eps, h->dprev, &h->dev->have_prev, (T*)h->Mc, (T*)h->Mp,
-                                         &h->dev->r, &h->dev->flags, h->dev->rep);
-  TRY(post_launch(h));
+  if (h->t2_pending) {  // Mc = T2 (U_B)_K, Mp = T2 (U_B)_K diag(d/sigma)
+    shrink_kernel<double><<<1, 1024, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec, C,
+                                                eps, h->dprev, &h->dev->have_prev, h->McD, h->MpD, &h->dev->r,
+                                                &h->dev->flags, h->dev->rep);
+    TRY(post_launch(h));
+    TRY(gemm_ll<T>(h, h->T2d, 0, h->McD, 0, (T*)h->Mc));
+    TRY(gemm_ll<T>(h, h->T2d, 0, h->MpD, 0, (T*)h->Mp));
+  } else {
+    shrink_kernel<T><<<1, 1024, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec,
+                                           C, eps, h->dprev, &h->dev->have_prev, (T*)h->Mc, (T*)h->Mp,
+                                           &h->dev->r, &h->dev->flags, h->dev->rep);
+    TRY(post_launch(h));
+  }
   TRY(apply_fast<T>(h, (const T*)h->Q, h->m, (const T*)h->Mc, (T*)h->Qt));
   TRY(apply_fast<T>(h, (const T*)h->Z, h->n, (const T*)h->Mp, (T*)h->Wt));
   return FRSVT_OK;
@@ -877,7 +940,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->E2b, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -945,6 +1008,12 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
                 {(void**)&h->partd, h->partd_elems * sizeof(double)},
                 {(void**)&h->redpart, h->redpart_elems * sizeof(double)},
                 {(void**)&h->G, sizeof(double) * l * l},
+                {(void**)&h->E2b, sizeof(double) * l * l},
+                {(void**)&h->T2d, sizeof(double) * l * l},
+                {(void**)&h->Hd, sizeof(double) * l * l},
+                {(void**)&h->McD, sizeof(double) * l * l},
+                {(void**)&h->MpD, sizeof(double) * l * l},
+                {(void**)&h->lwd, sizeof(int) * (FRSVT_LMAX + 4)},
                 {(void**)&h->UB, sizeof(double) * l * l},
                 {(void**)&h->sigma, sizeof(double) * FRSVT_LMAX},
                 {(void**)&h->dprev, sizeof(double) * FRSVT_LMAX},
@@ -978,6 +1047,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
+    const char* e3 = getenv("FRSVT_LOWDIN");
+    h->lowdin = !(e3 && e3[0] == '0');
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
@@ -998,6 +1069,16 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   set_smem_attrs<double>();
   cudaFuncSetAttribute(small2_kernel<SM2_EIG, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)small2_smem_bytes(FRSVT_LMAX, SM2_EIG));
+  cudaFuncSetAttribute(sgemm64_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)lowdin_smem_bytes(FRSVT_LMAX));
+  cudaFuncSetAttribute(sgemm64_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)lowdin_smem_bytes(FRSVT_LMAX));
+  cudaFuncSetAttribute(lowdin_sq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)lowdin_smem_bytes(FRSVT_LMAX));
+  cudaFuncSetAttribute(lowdin_series_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)lowdin_smem_bytes(FRSVT_LMAX));
+  cudaFuncSetAttribute(lowdin_series_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)lowdin_smem_bytes(FRSVT_LMAX));
   cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)jacobi_eig_smem_bytes(FRSVT_LMAX));
   cudaFuncSetAttribute(eig_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1243,6 +1324,22 @@ frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl,
   *ms = t / reps;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_debug_chol(frsvt_handle* h, const double* G, void* T, int32_t* s, unsigned long long* stamps) {
+  if (!h || !G || !T) return FRSVT_EINVAL;
+  CK(cudaMemcpyAsync(h->G, G, sizeof(double) * h->l * h->l, cudaMemcpyDeviceToDevice, h->st));
+  const double tol = h->esz == 4 ? 1e-12 : 1e-13;
+  if (h->esz == 4)
+    orth_chol_kernel<float><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(h->G, h->l, tol, (float*)T,
+                                                                                &h->dev->s, &h->dev->flags, stamps);
+  else
+    orth_chol_kernel<double><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(h->G, h->l, tol, (double*)T,
+                                                                                 &h->dev->s, &h->dev->flags, stamps);
+  TRY(post_launch(h));
+  CK(cudaStreamSynchronize(h->st));
+  if (s) CK(cudaMemcpy(s, &h->dev->s, sizeof(int), cudaMemcpyDeviceToHost));
   return FRSVT_OK;
 }
 

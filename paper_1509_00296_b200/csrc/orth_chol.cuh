@@ -21,8 +21,10 @@ namespace frsvt {
 constexpr int OC_THREADS = 256;
 
 __host__ __device__ constexpr size_t orth_chol_smem_bytes(int l) {
-  // S (l*l) + packed T~ (l(l+1)/2) + dsc (l) doubles; keep (l) ints
-  return ((size_t)l * l + (size_t)l * (l + 1) / 2 + (size_t)l) * sizeof(double) + (size_t)l * sizeof(int) + 64;
+  // S (l*(l+1): Schur complement, then the dense inverse with stride l+1) +
+  // packed R (l(l+1)/2) + dsc (l) + W scratch (3 x 32 x 32) doubles; keep (l) ints
+  return ((size_t)l * (l + 1) + (size_t)l * (l + 1) / 2 + (size_t)l + 3 * 1024) * sizeof(double) +
+         (size_t)l * sizeof(int) + 64;
 }
 
 __device__ __forceinline__ int oc_pk(int i, int j) { return j * (j + 1) / 2 + i; }  // packed upper, i <= j
@@ -30,12 +32,26 @@ __device__ __forceinline__ int oc_pk(int i, int j) { return j * (j + 1) / 2 + i;
 template <typename Tq>
 __global__ void __launch_bounds__(OC_THREADS, 1)
 orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict__ T, int* __restrict__ s_out,
-                 int* __restrict__ flags) {
+                 int* __restrict__ flags, unsigned long long* __restrict__ prof = nullptr,
+                 const int* __restrict__ skip = nullptr) {
+  // skip (nullable): a device flag set when the Loewdin path already produced T
+  if (skip && *skip) return;
+  // prof (test hook, nullable): %globaltimer stamps at phase boundaries
+#define OC_STAMP(k)                                                                  \
+  do {                                                                               \
+    if (prof && threadIdx.x == 0) {                                                  \
+      unsigned long long t_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+      prof[k] = t_;                                                                  \
+    }                                                                                \
+  } while (0)
+  OC_STAMP(0);
   extern __shared__ double ocs[];
   double* S = ocs;                                  // l*l row-major; R overwrites the upper triangle
-  double* Tt = S + (size_t)l * l;                   // packed T~
+  double* Tt = S + (size_t)l * (l + 1);             // packed R (after the factorisation)
   double* dsc = Tt + (size_t)l * (l + 1) / 2;
-  int* keep = (int*)(dsc + l);
+  double* Wsc = dsc + l;                            // 3 x 32 x 32 block products
+  int* keep = (int*)(Wsc + 3 * 1024);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tid & 15, ty = tid >> 4;
 
@@ -52,6 +68,7 @@ orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict
   }
   __syncthreads();
 
+  OC_STAMP(1);
   const int nb = (l + 15) >> 4;
   for (int P = 0; P < nb; ++P) {
     const int k0 = 16 * P, k1 = min(k0 + 16, l);
@@ -88,6 +105,7 @@ orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict
       }
     }
     __syncthreads();
+    if (P == 0) OC_STAMP(2);
     // (2) panel rows over the trailing columns, one thread per column, in
     //     registers: R[j][c] = (S[j][c] - sum_{k0<=t<j} R[t][j] R[t][c]) / R[j][j]
     for (int c = k1 + tid; c < l; c += OC_THREADS) {
@@ -109,6 +127,7 @@ orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict
         if (k0 + j < k1) S[(size_t)(k0 + j) * l + c] = v[j];
     }
     __syncthreads();
+    if (P == 0) OC_STAMP(3);
     // (3) trailing update (upper triangle): S[c1][c2] -= sum_{t in panel} R[t][c1] R[t][c2]
     const int w = l - k1;
     if (w > 0) {
@@ -144,65 +163,90 @@ orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict
     __syncthreads();
   }
 
-  // T~ = R^{-1} on the kept set (dropped rows/columns are zero): 16 x 16 blocks.
-  for (int I = warp; I < nb; I += OC_THREADS / 32) {
-    // lane c (< 16) owns column j = 16 I + c of T~_II, kept in registers;
-    // R_II rows are broadcast reads from shared memory
-    const int c = lane & 15, i0 = 16 * I;
-    const int j = i0 + c;
-    double tcol[16];
+  OC_STAMP(4);
+  // T~ = R^{-1} on the kept set (dropped rows/columns are zero), by 32 x 32
+  // blocks: (A) the diagonal blocks, one warp each, back substitution in
+  // registers (lane = column); (B) block diagonals d = 1.. in parallel:
+  // W_IJ = sum_{I<K<=J} R_IK T_KJ, T_IJ = -T_II W_IJ. R is first moved to
+  // packed storage so that S can hold the dense inverse (row stride l + 1).
+  for (int idx = tid; idx < l * l; idx += OC_THREADS) {
+    const int i = idx / l, j = idx % l;
+    if (j >= i) Tt[oc_pk(i, j)] = keep[i] ? S[(size_t)i * l + j] : 0.0;
+  }
+  __syncthreads();
+  double* Tn = S;  // dense inverse, Tn[i * (l + 1) + j]
+  const int ldt = l + 1;
+  for (int idx = tid; idx < l * ldt; idx += OC_THREADS) Tn[idx] = 0.0;
+  __syncthreads();
+  const int NB = (l + 31) >> 5;
+  if (warp < NB) {
+    const int c = lane, w0 = 32 * warp, j = w0 + c;
+    double x[32];
 #pragma unroll
-    for (int r = 15; r >= 0; --r) {
-      const int i = i0 + r;
-      double u = (r == c) ? 1.0 : 0.0;
+    for (int r = 31; r >= 0; --r) {
+      const int i = w0 + r;
+      double v = 0.0;
+      if (i < l && keep[i] && r <= c && j < l && keep[j]) {
+        double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
 #pragma unroll
-      for (int t = r + 1; t < 16; ++t)
-        if (t <= c && i0 + t < l) u = fma(-S[(size_t)i * l + i0 + t], tcol[t], u);
-      const bool ok = (r <= c) && (j < l) && (i < l) && keep[i] && keep[j];
-      tcol[r] = ok ? u / S[(size_t)i * l + i] : 0.0;
+        for (int k = r + 1; k < 32; k += 2) {
+          if (w0 + k < l) s0 = fma(-Tt[oc_pk(i, w0 + k)], x[k], s0);
+          if (k + 1 < 32 && w0 + k + 1 < l) s1 = fma(-Tt[oc_pk(i, w0 + k + 1)], x[k + 1], s1);
+        }
+        v = (s0 + s1) / Tt[oc_pk(i, i)];
+      }
+      x[r] = v;
     }
-    if (lane < 16 && j < l) {
+    if (j < l) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r <= c) Tt[oc_pk(i0 + r, j)] = tcol[r];
+      for (int r = 0; r < 32; ++r)
+        if (w0 + r < l) Tn[(size_t)(w0 + r) * ldt + j] = x[r];
     }
   }
   __syncthreads();
-  for (int d = 1; d < nb; ++d) {
-    for (int I = 0; I + d < nb; ++I) {
-      const int J = I + d;
-      const int gi = 16 * I + ty, gj = 16 * J + tx;
-      double wv = 0.0;
+  OC_STAMP(5);
+  for (int d = 1; d < NB; ++d) {
+    const int npairs = NB - d;
+    // (B1) W_IJ = sum_{K = I+1..J} R_IK T_KJ  (thread: b fastest -> broadcast R, stride-1 T)
+    for (int o = tid; o < npairs * 1024; o += OC_THREADS) {
+      const int pr = o >> 10, a = (o >> 5) & 31, b = o & 31;
+      const int I = pr, J = pr + d;
+      const int gi = 32 * I + a, gj = 32 * J + b;
+      double w = 0.0, w2 = 0.0;
       if (gi < l && gj < l) {
-        // W = sum_{t = 16(I+1)}^{gj} R[gi][t] T~[t][gj]
-        double w1 = 0.0, w2 = 0.0, w3 = 0.0;
-        int t = 16 * (I + 1);
-        for (; t + 3 <= gj; t += 4) {
-          wv = fma(S[(size_t)gi * l + t], Tt[oc_pk(t, gj)], wv);
-          w1 = fma(S[(size_t)gi * l + t + 1], Tt[oc_pk(t + 1, gj)], w1);
-          w2 = fma(S[(size_t)gi * l + t + 2], Tt[oc_pk(t + 2, gj)], w2);
-          w3 = fma(S[(size_t)gi * l + t + 3], Tt[oc_pk(t + 3, gj)], w3);
+        const int t1 = min(gj, l - 1);
+        int t = 32 * (I + 1);
+        for (; t + 1 <= t1; t += 2) {
+          w = fma(Tt[oc_pk(gi, t)], Tn[(size_t)t * ldt + gj], w);
+          w2 = fma(Tt[oc_pk(gi, t + 1)], Tn[(size_t)(t + 1) * ldt + gj], w2);
         }
-        for (; t <= gj; ++t) wv = fma(S[(size_t)gi * l + t], Tt[oc_pk(t, gj)], wv);
-        wv = (wv + w1) + (w2 + w3);
+        if (t <= t1) w = fma(Tt[oc_pk(gi, t)], Tn[(size_t)t * ldt + gj], w);
       }
-      __syncthreads();
-      if (gi < l && gj < l) Tt[oc_pk(gi, gj)] = wv;
-      __syncthreads();
-      double v = 0.0;
-      if (gi < l && gj < l) {
-        const int i1 = min(16 * I + 16, l);
-        for (int t = gi; t < i1; ++t) v = fma(Tt[oc_pk(gi, t)], Tt[oc_pk(t, gj)], v);
-      }
-      __syncthreads();
-      if (gi < l && gj < l) Tt[oc_pk(gi, gj)] = keep[gj] ? -v : 0.0;
-      __syncthreads();
+      Wsc[pr * 1024 + a * 32 + b] = w + w2;
     }
+    __syncthreads();
+    // (B2) T_IJ = -T_II W_IJ
+    for (int o = tid; o < npairs * 1024; o += OC_THREADS) {
+      const int pr = o >> 10, a = (o >> 5) & 31, b = o & 31;
+      const int I = pr, J = pr + d;
+      const int gi = 32 * I + a, gj = 32 * J + b;
+      if (gi < l && gj < l) {
+        double v = 0.0, v2 = 0.0;
+        for (int t = a; t < 32; t += 2) {
+          v = fma(Tn[(size_t)gi * ldt + 32 * I + t], Wsc[pr * 1024 + t * 32 + b], v);
+          if (t + 1 < 32) v2 = fma(Tn[(size_t)gi * ldt + 32 * I + t + 1], Wsc[pr * 1024 + (t + 1) * 32 + b], v2);
+        }
+        Tn[(size_t)gi * ldt + gj] = -(v + v2);
+      }
+    }
+    __syncthreads();
   }
+  OC_STAMP(6);
   for (int idx = tid; idx < l * l; idx += OC_THREADS) {
     const int o = idx % l, j = idx / l;  // T[o + j*l]
-    T[idx] = (Tq)((o <= j) ? dsc[o] * Tt[oc_pk(o, j)] : 0.0);
+    T[idx] = (Tq)((o <= j) ? dsc[o] * Tn[(size_t)o * ldt + j] : 0.0);
   }
+  OC_STAMP(7);
   if (tid == 0) {
     int s = 0;
     for (int i = 0; i < l; ++i) s += keep[i];

@@ -405,6 +405,7 @@ __global__ void shrink_kernel(const double* __restrict__ sigma, const double* __
   __syncthreads();
   for (int i = tid; i < l; i += blockDim.x) d_prev[i] = d_sh[i];
   const int r = r_sh;
+#pragma unroll 4
   for (int idx = tid; idx < l * l; idx += blockDim.x) {
     const int row = idx % l, j = idx / l;
     double vc = 0.0, vp = 0.0;

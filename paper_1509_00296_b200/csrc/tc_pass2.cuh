@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
   const int mtiles = (Mtot + 127) / 128;
   const int64_t total = (int64_t)mtiles * nch;
   const int tile = blockIdx.x;
+  const int cgrp = blockIdx.y, ngrp = gridDim.y;  // column groups of the tile
   if (threadIdx.x == 0) {
     const int64_t t0 = (int64_t)tile * nch, t1 = t0 + nch;
     // CTAs whose range intersects [t0, t1)
@@ -516,8 +517,10 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
   const int nc = ncov;
   if (nc == 0) return;  // written directly by the pass
   const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
-  for (int idx = threadIdx.x; idx < 128 * Nvalid; idx += blockDim.x) {
-    const int row = idx & 127, c = idx >> 7;
+  const int cpg = (Nvalid + ngrp - 1) / ngrp;
+  const int cb = cgrp * cpg, ce = min(Nvalid, cb + cpg);
+  for (int idx = threadIdx.x; idx < 128 * (ce - cb); idx += blockDim.x) {
+    const int row = idx & 127, c = cb + (idx >> 7);
     const int gm = tile * 128 + row;
     if (gm >= Mtot) continue;
     if (rp_dev && c < rsh) {  // carried column
