@@ -427,11 +427,20 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
       !make_map(&mWl, h->WtTl, Kp, h->n, Kp, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return FRSVT_ECUDA;
   const int rbs = (int)cdiv(h->m, 128), ntiles = (int)cdiv(h->n, 128);
-  int cs = rbs >= 2 * 148 ? 1 : (int)cdiv(2 * 148, rbs);
-  if (cs > ntiles) cs = ntiles;
-  const int tpc = (int)cdiv(ntiles, cs);
-  cs = (int)cdiv(ntiles, tpc);
-  dim3 grid((unsigned)rbs, (unsigned)cs);
+  const int W = h->nsm;
+  int nfull, rem, sp;
+  if (rbs >= W) {
+    nfull = (rbs / W) * W;
+    rem = rbs - nfull;
+    sp = rem ? (W / rem) : 1;
+  } else {
+    nfull = 0;
+    rem = rbs;
+    sp = (int)cdiv(2 * W, rbs);
+  }
+  if (sp > ntiles) sp = ntiles;
+  if (sp < 1) sp = 1;
+  dim3 grid((unsigned)(nfull + rem * sp));
   const size_t smem = tc::ComposeSmem::total();
   static bool attr[3] = {false, false, false};
 #define FRSVT_LAUNCH_CMP(EPIV)                                                                                  \
@@ -441,14 +450,14 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
       attr[EPIV] = true;                                                                                        \
     }                                                                                                           \
     tc::tc_compose_kernel<EPIV><<<grid, tc::CMP_THREADS, smem, h->st>>>(mQh, mQl, mWh, mWl, (int)h->m, (int)h->n, \
-                                                                        &h->dev->r, tpc, X, ldx, D, A, E, ld,    \
+                                                                        &h->dev->r, nfull, sp, X, ldx, D, A, E, ld,    \
                                                                         h->dev->mu, rho, lambda, h->redpart);    \
   } while (0)
   if (epi == tc::EPI_STORE) FRSVT_LAUNCH_CMP(tc::EPI_STORE);
   else if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP(tc::EPI_ALM);
   else FRSVT_LAUNCH_CMP(tc::EPI_FINAL);
 #undef FRSVT_LAUNCH_CMP
-  if (nparts) *nparts = (int)(grid.x * grid.y);
+  if (nparts) *nparts = (int)grid.x;
   return post_launch(h);
 }
 

@@ -53,7 +53,7 @@ template <int EPI>
 __global__ void __launch_bounds__(CMP_THREADS, 1)
 tc_compose_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_constant__ CUtensorMap mapQl,
                   const __grid_constant__ CUtensorMap mapWh, const __grid_constant__ CUtensorMap mapWl, int m, int n,
-                  const int* __restrict__ r_dev, int tiles_per_cta, float* __restrict__ X, int64_t ldx,
+                  const int* __restrict__ r_dev, int nfull, int sp, float* __restrict__ X, int64_t ldx,
                   const float* __restrict__ D, float* __restrict__ Aop, float* __restrict__ E, int64_t ld,
                   const double* __restrict__ mu, double rho, double lambda, double* __restrict__ part) {
   constexpr uint32_t CB = ComposeSmem::chunk_bytes;
@@ -72,10 +72,23 @@ tc_compose_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_consta
   __shared__ double red[CMP_THREADS / 32];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rb = blockIdx.x;                       // 128-row block
+  // CTA -> work: the first nfull CTAs take one whole 128-row block each (full
+  // waves, all CTAs of a wave sweep the same column tiles in step: long
+  // contiguous DRAM runs per column); the remaining row blocks are split into
+  // sp column ranges so the last wave is not a tail of a few CTAs
   const int ntiles = (n + 127) / 128;
-  const int jt0 = blockIdx.y * tiles_per_cta;
-  const int jt1 = min(ntiles, jt0 + tiles_per_cta);
+  int rb, jt0, jt1;
+  if ((int)blockIdx.x < nfull) {
+    rb = blockIdx.x;
+    jt0 = 0;
+    jt1 = ntiles;
+  } else {
+    const int e = blockIdx.x - nfull;
+    const int tpc = (ntiles + sp - 1) / sp;
+    rb = nfull + e / sp;
+    jt0 = (e % sp) * tpc;
+    jt1 = min(ntiles, jt0 + tpc);
+  }
   const int r = *r_dev;
   const int nk = (r + BK - 1) / BK;                // K chunks actually used (r <= Kp)
 
@@ -245,7 +258,7 @@ tc_compose_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_consta
   if (EPI != EPI_STORE && threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 4; w < CMP_THREADS / 32; ++w) s += red[w];
-    part[blockIdx.x + (int64_t)gridDim.x * blockIdx.y] = s;
+    part[blockIdx.x] = s;
   }
   if (warp == 2) {
     tc_fence_after();
