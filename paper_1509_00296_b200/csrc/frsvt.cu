@@ -18,6 +18,7 @@
 #include "eig_jacobi.cuh"
 #include "orth_chol.cuh"
 #include "lowdin.cuh"
+#include "chol_fast.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
 #include "tc_pass2.cuh"
@@ -72,6 +73,8 @@ struct frsvt_handle {
   int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
   double* E2b;       // Loewdin workspace E^2 (l x l fp64)
+  double* Rf;        // first-pass CholeskyQR factor R' (l x l row-major fp64)
+  int fastchol;      // 1: chol_rows_kernel + trsm_rows_kernel (fp32 handles)
   double *T2d, *Hd, *McD, *MpD;  // fp64 l x l: pending second CholeskyQR factor and fold scratch
   int t2_pending;    // 1: h->Q holds Q1 and the basis is Q1 T2d (T2d folded into G, Mc, Mp)
   int* lwd;          // device ints: [0] ok flag, [2..3] max|E| (u64)
@@ -567,8 +570,30 @@ frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, 
 // matters next (the next orthonormalisation follows: the sketch before a
 // power step, Z = A^T Q before A Z), so the second pass runs only on the
 // final basis of the range finder (orth_final).
+template <int NB>
+frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float* Out) {
+  const size_t smem = (size_t)(32 * NB) * (32 * NB + 1) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(trsm_rows_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  trsm_rows_kernel<NB><<<(unsigned)cdiv(rows, 128), 128, smem, h->st>>>(In, rows, rows, h->Rf, h->l, Out, rows);
+  return post_launch(h);
+}
+
 template <typename T>
 frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
+  if constexpr (sizeof(T) == 4) {
+    if (h->fastchol) {  // R' by the register-resident Cholesky, Q1 = Y R'^{-1} by row-parallel TRSM
+      TRY(gram<T>(h, In, rows, rows, sharded));
+      chol_rows_kernel<<<1, CHR_THREADS, 0, h->st>>>(h->G, h->l, 1e-12, h->Rf, &h->dev->s, &h->dev->flags, nullptr);
+      TRY(post_launch(h));
+      if (h->l <= 32) return trsm_rows_nb<1>(h, (const float*)In, rows, (float*)Out);
+      if (h->l <= 64) return trsm_rows_nb<2>(h, (const float*)In, rows, (float*)Out);
+      return trsm_rows_nb<4>(h, (const float*)In, rows, (float*)Out);
+    }
+  }
   TRY(gram<T>(h, In, rows, rows, sharded));
   TRY(chol<T>(h, (T*)h->T1));
   return apply_small<T>(h, In, rows, rows, (const T*)h->T1, Out, rows);
@@ -949,7 +974,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->E2b, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1018,6 +1043,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
                 {(void**)&h->redpart, h->redpart_elems * sizeof(double)},
                 {(void**)&h->G, sizeof(double) * l * l},
                 {(void**)&h->E2b, sizeof(double) * l * l},
+                {(void**)&h->Rf, sizeof(double) * l * l},
                 {(void**)&h->T2d, sizeof(double) * l * l},
                 {(void**)&h->Hd, sizeof(double) * l * l},
                 {(void**)&h->McD, sizeof(double) * l * l},
@@ -1058,6 +1084,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->pass2 = !(e && e[0] == '0');
     const char* e3 = getenv("FRSVT_LOWDIN");
     h->lowdin = !(e3 && e3[0] == '0');
+    const char* e4 = getenv("FRSVT_FASTCHOL");  // experimental (slower so far): opt in with 1
+    h->fastchol = (e4 && e4[0] == '1');
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
