@@ -106,11 +106,7 @@ def _dist():
     return 1, 0, local, None
 
 
-def shard(m, ws, rank):
-    base, rem = divmod(m, ws)
-    m_loc = base + (1 if rank < rem else 0)
-    row0 = rank * base + min(rank, rem)
-    return row0, m_loc
+from paper_1509_00296_b200.sharding import exchange_unique_id, shard  # noqa: E402
 
 
 def _oracle_sample(cfg_name, rows_sample):
@@ -208,11 +204,7 @@ def main():
     del data
     torch.cuda.empty_cache()
     n, l = cfg.n, cfg.l
-    nccl_id = None
-    if ws > 1:
-        obj = [P.Frsvt.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    nccl_id = exchange_unique_id(dist, rank, P.Frsvt.unique_id) if ws > 1 else None
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         h = P.Frsvt(m_loc, n, l, cfg.q, rp=cfg.rp, dtype=torch.float32, seed=cfg.seed, stream=stream,
