@@ -119,6 +119,7 @@ tc_compose_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_consta
       prefetch_tmap(&mapQl);
       prefetch_tmap(&mapWh);
       prefetch_tmap(&mapWl);
+      const uint64_t wpol = l2_policy_evict_last();  // Wt tiles are re-read by every row block
       mbar_expect_tx(qfull, 2 * CB * nk);
       for (int kc = 0; kc < nk; ++kc) {
         tma_load_2d(sQh + kc * CB, &mapQh, qfull, kc * BK, rb * 128);
@@ -131,8 +132,8 @@ tc_compose_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_consta
           const uint32_t ph = (it / CMP_WSTAGES) & 1;
           mbar_wait(&wempty[s], ph ^ 1);
           mbar_expect_tx(&wfull[s], 2 * CB);
-          tma_load_2d(sWh + s * CB, &mapWh, &wfull[s], kc * BK, jt * 128);
-          tma_load_2d(sWl + s * CB, &mapWl, &wfull[s], kc * BK, jt * 128);
+          tma_load_2d_hint(sWh + s * CB, &mapWh, &wfull[s], kc * BK, jt * 128, wpol);
+          tma_load_2d_hint(sWl + s * CB, &mapWl, &wfull[s], kc * BK, jt * 128, wpol);
         }
       }
     }

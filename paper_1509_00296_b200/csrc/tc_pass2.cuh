@@ -238,6 +238,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     // A producer (HBM stream, deep ring)
     if (lane == 0 && nloc > 0) {
       prefetch_tmap(&mapA);
+      const uint64_t pol = l2_policy_evict_first();
       for (int i = 0; i < nloc; ++i) {
         const int64_t g = g0 + i;
         const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
@@ -247,9 +248,9 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         p2_stamp(dbg, out, 0, i, nloc);
         mbar_expect_tx(&fulla[s], A_BYTES);
         if (MODE == MODE_AX)
-          tma_load_2d(sA + s * A_BYTES, &mapA, &fulla[s], tile * 128, kc);
+          tma_load_2d_hint(sA + s * A_BYTES, &mapA, &fulla[s], tile * 128, kc, pol);
         else
-          tma_load_2d(sA + s * A_BYTES, &mapA, &fulla[s], kc, tile * 128);
+          tma_load_2d_hint(sA + s * A_BYTES, &mapA, &fulla[s], kc, tile * 128, pol);
       }
       p2_cta_stamp(dbg, out, 1);
     }
@@ -258,6 +259,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     if (lane == 0 && nloc > 0) {
       prefetch_tmap(&mapBh);
       prefetch_tmap(&mapBl);
+      const uint64_t pol = l2_policy_evict_last();
       for (int i = 0; i < nloc; ++i) {
         const int64_t g = g0 + i;
         const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
@@ -270,8 +272,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           continue;
         }
         mbar_expect_tx(&fullb[s], btx);
-        tma_load_2d(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0);
-        tma_load_2d(sB + s * B_BYTES + BH_BYTES, &mapBl, &fullb[s], 2 * kc, 0);
+        tma_load_2d_hint(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0, pol);
+        tma_load_2d_hint(sB + s * B_BYTES + BH_BYTES, &mapBl, &fullb[s], 2 * kc, 0, pol);
       }
     }
   } else if (warp == 1) {
