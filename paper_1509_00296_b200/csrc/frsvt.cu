@@ -71,6 +71,7 @@ struct frsvt_handle {
   int64_t ldxs, ldqs;
   int use_tc;
   int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
+  int p2cl;          // stream-K pass cluster size (1, or 2: B stages multicast to a CTA pair)
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
   double* E2b;       // Loewdin workspace E^2 (l x l fp64)
   double* Rf;        // first-pass CholeskyQR factor R' (l x l row-major fp64)
@@ -347,27 +348,50 @@ frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q
 }
 
 // ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
+template <int MODE, int NP, int CL>
+frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
+                          const int* rp_dev) {
+  const size_t smem = tc::Pass2Smem::total(CL > 1 ? 128 : h->l);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(tc::tc_pass2_kernel<MODE, NP, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tc::Pass2Smem::total(FRSVT_LMAX)));
+    attr_set = true;
+  }
+  const int mtiles = (int)cdiv(Mtot, 128);
+  const int64_t total = (int64_t)cdiv(mtiles, CL) * cdiv(Ktot, tc::BK);
+  const int Gmax = h->nsm / CL;
+  const int G = (int)(total < Gmax ? total : Gmax);  // work groups (clusters)
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(G * CL));
+  lc.blockDim = dim3(tc::P2_THREADS);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
+                        ldadd, h->skpart, rp_dev, dbg));
+  TRY(post_launch(h));
+  if (dbg & 96) return FRSVT_OK;
+  // one block per (tile, 8-column group): enough independent loads in flight
+  tc::tc_fixup_kernel<NP, CL><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
+      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
+  return post_launch(h);
+}
+
 template <int MODE, int NP>
 frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
                           const int* rp_dev = nullptr) {
-  const size_t smem = tc::Pass2Smem::total();
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(tc::tc_pass2_kernel<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
-  const int mtiles = (int)cdiv(Mtot, 128);
-  const int64_t total = (int64_t)mtiles * cdiv(Ktot, tc::BK);
-  const int G = (int)(total < h->nsm ? total : h->nsm);
-  tc::tc_pass2_kernel<MODE, NP><<<G, tc::P2_THREADS, smem, h->st>>>(mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo,
-                                                                    add, ldadd, h->skpart, rp_dev, dbg);
-  TRY(post_launch(h));
-  if (dbg & 96) return FRSVT_OK;
-  // one block per (tile, 8-column group): enough independent loads in flight
-  tc::tc_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
-      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
-  return post_launch(h);
+  if (h->p2cl == 2)
+    return launch_p2_cl<MODE, NP, 2>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+  return launch_p2_cl<MODE, NP, 1>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev);
 }
 
 // out (Mtot x l) = op(A) * B, B (Ktot x l, ld ldb) the small operand:
@@ -383,7 +407,7 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   tc::split_tf32_bf16x2_kernel<<<grid1d(kx * h->l), 256, 0, h->st>>>(B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
   TRY(post_launch(h));
   CUtensorMap mA, mBh, mBl;
-  const uint32_t nb = (uint32_t)h->l;
+  const uint32_t nb = h->p2cl == 2 ? 64u : (uint32_t)h->l;  // clustered: each CTA loads a 64-row half
   bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
                                   : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1086,6 +1110,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
+    const char* e5 = getenv("FRSVT_P2CL");
+    h->p2cl = (e5 && e5[0] == '1') ? 1 : 2;
     const char* e3 = getenv("FRSVT_LOWDIN");
     h->lowdin = !(e3 && e3[0] == '0');
     const char* e4 = getenv("FRSVT_FASTCHOL");  // experimental (slower so far): opt in with 1

@@ -51,8 +51,11 @@
 namespace frsvt {
 namespace tc {
 
-constexpr int P2_ASTAGES = 5;  // A ring (16 KB stages; released by the converters)
-constexpr int P2_BSTAGES = 4;  // B ring (32 KB stages; released by the MMA; L2 latency ~2400 cycles under load)
+constexpr int P2_ASTAGES = 4;  // A ring (16 KB stages; released by the converters)
+// B ring: released by the MMA. Its depth must cover MMA completion (~700
+// cycles) + the L2 latency of the small operand under the A stream (~1900
+// cycles, clock64 stamps): 5 stages of (roundup8(l) rows x 256 B)
+constexpr int P2_BSTAGES = 5;
 constexpr int P2_TSTAGES = 4;  // TMEM A ring (64 columns per stage: a_h tf32 | bf16 a_h | bf16 a_l)
 constexpr int P2_SEG = 8;      // chunks accumulated in TMEM before a flush
 constexpr int P2_THREADS = 640;
@@ -63,8 +66,10 @@ struct Pass2Smem {
   static constexpr uint32_t bh_bytes = 128u * BK * 4u;        // 16 KB (N <= 128 rows)
   static constexpr uint32_t bx_bytes = 128u * 2 * BK * 2u;    // 16 KB: bf16 [b_l | b_h], 64 K per row
   static constexpr uint32_t b_bytes = bh_bytes + bx_bytes;    // 32 KB
-  static constexpr size_t total() {
-    return 1024 + (size_t)P2_ASTAGES * a_bytes + (size_t)P2_BSTAGES * b_bytes + 512;
+  // one B stage for nb valid rows (128B-swizzle atoms are 8 rows = 1 KB)
+  __host__ __device__ static constexpr uint32_t b_stage(int nb) { return 2u * (uint32_t)((nb + 7) / 8) * 1024u; }
+  __host__ __device__ static constexpr size_t total(int nb) {
+    return 1024 + (size_t)P2_ASTAGES * a_bytes + (size_t)P2_BSTAGES * b_stage(nb) + 512;
   }
 };
 
@@ -124,6 +129,30 @@ __device__ __forceinline__ void p2_stamp(int dbg, float* out, int ev, int i, int
   }
 }
 
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA 2D load multicast to the CTAs in ctaMask (same smem offset in each; each
+// destination's mbarrier at the same offset receives the complete_tx)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint "
+      "[%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(pred));
@@ -157,7 +186,12 @@ struct P2Walk {
   }
 };
 
-template <int MODE, int NP>
+// CL = 2: the CTAs of a 2-CTA cluster take the two 128-row tiles of a
+// 256-row pair over the same K chunks; each loads half of every B stage and
+// multicasts it to both (halving the B traffic through L2, which the passes
+// were bound by: A + B re-reads ~ 2.9x A at the ~12 TB/s LTS cap), and a
+// B stage is reused only after both CTAs' MMAs consumed it.
+template <int MODE, int NP, int CL>
 __global__ void __launch_bounds__(P2_THREADS, 1)
 tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
                 const __grid_constant__ CUtensorMap mapBl, int Mtot, int Ktot, int Nvalid, int nbrows,
@@ -171,23 +205,20 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   // bit 3 no bf16 MMAs, bit 4 no a_lo MMAs, bit 5 clock64 stamps of CTA 0 into out (output invalid)
   static_assert(NP % 16 == 0 && NP >= 32 && NP <= 128, "N tile");
   constexpr uint32_t A_BYTES = Pass2Smem::a_bytes;
-  constexpr uint32_t BH_BYTES = Pass2Smem::bh_bytes;
-  constexpr uint32_t B_BYTES = Pass2Smem::b_bytes;
+  const uint32_t B_BYTES = Pass2Smem::b_stage(CL > 1 ? 128 : nbrows);  // Bh | Bx, each rows x 128 B
+  const uint32_t BHB = B_BYTES / 2;
   constexpr int HALF = NP / 2;  // columns per flush warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // P2_ASTAGES x 16 KB
-  uint8_t* sB = smem + P2_ASTAGES * A_BYTES;            // P2_BSTAGES x 24 KB (Bh 16 KB | Bl 8 KB)
+  uint8_t* sB = smem + P2_ASTAGES * A_BYTES;            // P2_BSTAGES x B_BYTES
   uint64_t* fulla = (uint64_t*)(sB + P2_BSTAGES * B_BYTES);
   uint64_t* emptya = fulla + P2_ASTAGES;
   uint64_t* fullb = emptya + P2_ASTAGES;
   uint64_t* emptyb = fullb + P2_BSTAGES;
   uint64_t* tfull = emptyb + P2_BSTAGES;
-  // one MMA-completion barrier per stage frees both the B stage and the TMEM
-  // A stage of a chunk (one tcgen05.commit per chunk)
-  static_assert(P2_BSTAGES == P2_TSTAGES, "B and TMEM rings share the completion barrier");
-  uint64_t* tempty = emptyb;
-  uint64_t* accfull = tfull + P2_TSTAGES;
+  uint64_t* tempty = tfull + P2_TSTAGES;
+  uint64_t* accfull = tempty + P2_TSTAGES;
   uint64_t* accempty = accfull + 2;
   uint32_t* tslot = (uint32_t*)(accempty + 2);
 
@@ -200,12 +231,16 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int nmma = min(NP, max(16, ((rp_dev ? nact : Nvalid) + 7) & ~7));
   const int nch = (Ktot + BK - 1) / BK;
   const int mtiles = (Mtot + 127) / 128;
-  const int64_t total = (int64_t)mtiles * nch;
-  const int G = gridDim.x, cta = blockIdx.x;
-  const int64_t g0 = p2_range_begin(total, G, cta), g1 = p2_range_begin(total, G, cta + 1);
+  const int mgroups = (mtiles + CL - 1) / CL;  // work tiles: CL row tiles each
+  const int64_t total = (int64_t)mgroups * nch;
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int G = gridDim.x / CL, cta = blockIdx.x, cgrp = blockIdx.x / CL;
+  const int64_t g0 = p2_range_begin(total, G, cgrp), g1 = p2_range_begin(total, G, cgrp + 1);
   const int nloc = (int)(g1 - g0);
-  // expected TMA bytes per B stage (B boxes are nbrows rows)
-  const uint32_t btx = (uint32_t)nbrows * BK * 4u + (uint32_t)nbrows * 2 * BK * 2u;
+  // expected TMA bytes per B stage (CL = 1: boxes of nbrows rows; CL = 2: both
+  // CTAs' 64-row halves, out-of-bounds rows zero-filled and counted)
+  const uint32_t brows = CL > 1 ? 128u : (uint32_t)nbrows;
+  const uint32_t btx = brows * BK * 4u + brows * 2 * BK * 2u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P2_ASTAGES; ++s) {
@@ -214,9 +249,12 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     }
     for (int s = 0; s < P2_BSTAGES; ++s) {
       mbar_init(&fullb[s], 1);
-      mbar_init(&emptyb[s], 1);
+      mbar_init(&emptyb[s], CL);
     }
-    for (int t = 0; t < P2_TSTAGES; ++t) mbar_init(&tfull[t], 8);
+    for (int t = 0; t < P2_TSTAGES; ++t) {
+      mbar_init(&tfull[t], 8);
+      mbar_init(&tempty[t], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], 8);
@@ -229,6 +267,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // barriers initialised before the partner multicasts into them
   tc_fence_after();
   const uint32_t tbase = *tslot;
   const uint32_t t_acc0 = tbase;     // accumulator buffer b at columns [128 b, 128 b + NP)
@@ -241,7 +280,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const uint64_t pol = l2_policy_evict_first();
       for (int i = 0; i < nloc; ++i) {
         const int64_t g = g0 + i;
-        const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
+        const int grp = (int)(g / nch), kc = (int)(g - (int64_t)grp * nch) * BK;
+        const int tile = grp * CL + crank;
         const int s = i % P2_ASTAGES;
         const uint32_t ph = (i / P2_ASTAGES) & 1;
         mbar_wait(&emptya[s], ph ^ 1);
@@ -262,7 +302,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const uint64_t pol = l2_policy_evict_last();
       for (int i = 0; i < nloc; ++i) {
         const int64_t g = g0 + i;
-        const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK;
+        const int grp = (int)(g / nch), kc = (int)(g - (int64_t)grp * nch) * BK;
         const int s = i % P2_BSTAGES;
         const uint32_t ph = (i / P2_BSTAGES) & 1;
         mbar_wait(&emptyb[s], ph ^ 1);
@@ -272,8 +312,14 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           continue;
         }
         mbar_expect_tx(&fullb[s], btx);
-        tma_load_2d_hint(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0, pol);
-        tma_load_2d_hint(sB + s * B_BYTES + BH_BYTES, &mapBl, &fullb[s], 2 * kc, 0, pol);
+        if (CL > 1) {  // my 64-row half of the stage, into both CTAs
+          const uint32_t ho = (uint32_t)crank * 64u * 128u;
+          tma_load_2d_mc(sB + s * B_BYTES + ho, &mapBh, &fullb[s], kc, 64 * crank, 0x3, pol);
+          tma_load_2d_mc(sB + s * B_BYTES + BHB + ho, &mapBl, &fullb[s], 2 * kc, 64 * crank, 0x3, pol);
+        } else {
+          tma_load_2d_hint(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0, pol);
+          tma_load_2d_hint(sB + s * B_BYTES + BHB, &mapBl, &fullb[s], 2 * kc, 0, pol);
+        }
       }
     }
   } else if (warp == 1) {
@@ -306,14 +352,16 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           if (leader) p2_stamp(dbg, out, 4, i, nloc);
           if (dbg & 1) {
             if (leader) {
-              mbar_arrive(&emptyb[s]);
+              if (CL > 1) tc_commit_mc(&emptyb[s], 0x3);
+              else mbar_arrive(&emptyb[s]);
+              mbar_arrive(&tempty[t]);
             }
             __syncwarp();
             continue;
           }
           const uint32_t st = sB_u + (uint32_t)s * B_BYTES;
           const uint64_t bh = desc_kmajor_sw128(st);
-          const uint64_t bx = desc_kmajor_sw128(st + BH_BYTES);
+          const uint64_t bx = desc_kmajor_sw128(st + BHB);
           const uint32_t a_hi = t_a + t * 64, a_x = a_hi + 32;
           if (leader) {
 #pragma unroll
@@ -328,7 +376,9 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                 mma_bf16_ts(acc, a_x + kk * 8, bx + koff, id_bf, 1u);
               }
             }
-            tc_commit(&emptyb[s]);
+            if (CL > 1) tc_commit_mc(&emptyb[s], 0x3);  // frees stage s in both CTAs
+            else tc_commit(&emptyb[s]);
+            tc_commit(&tempty[t]);
             p2_stamp(dbg, out, 5, i, nloc);
           }
           __syncwarp();
@@ -441,7 +491,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       ++piece;
       if (tl && !(dbg & 96)) {
         const bool whole = (tile_k0 == 0) && (k1 == nch);
-        const int gm = tile * 128 + row;
+        const int gm = (tile * CL + crank) * 128 + row;
         if (whole) {
           if (gm < Mtot) {
 #pragma unroll
@@ -473,6 +523,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   if (warp == 12 && lane == 0) p2_cta_stamp(dbg, out, 2);
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // the partner no longer multicasts into this CTA
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tbase, 512);
@@ -483,20 +534,24 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 // Tiles split between CTAs: out = sum of the covering CTAs' partial slots (in
 // CTA order) (+ add). One block per tile; the covering CTAs and their slots
 // are resolved once per block (gridDim of the pass G <= 256).
-template <int NP>
+template <int NP, int CL>
 __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
                                                        const float* __restrict__ part, float* __restrict__ out,
                                                        int64_t ldo, const float* __restrict__ add, int64_t ldadd,
                                                        const int* __restrict__ rp_dev) {
   __shared__ int64_t soff[256];
   __shared__ int ncov;
+  // G = number of work groups (clusters for CL = 2); group c's CTA for row
+  // tile t is c * CL + t % CL, its slots [cta][first|last segment]
   const int nch = (Ktot + BK - 1) / BK;
   const int mtiles = (Mtot + 127) / 128;
-  const int64_t total = (int64_t)mtiles * nch;
+  const int mgroups = (mtiles + CL - 1) / CL;
+  const int64_t total = (int64_t)mgroups * nch;
   const int tile = blockIdx.x;
+  const int wt = tile / CL, crank = tile % CL;
   const int cgrp = blockIdx.y, ngrp = gridDim.y;  // column groups of the tile
   if (threadIdx.x == 0) {
-    const int64_t t0 = (int64_t)tile * nch, t1 = t0 + nch;
+    const int64_t t0 = (int64_t)wt * nch, t1 = t0 + nch;
     // CTAs whose range intersects [t0, t1)
     int c0 = (int)((t0 * G) / total);
     while (c0 > 0 && p2_range_begin(total, G, c0) > t0) --c0;
@@ -510,7 +565,7 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
         const int64_t b = p2_range_begin(total, G, cc);
         if (p2_range_begin(total, G, cc + 1) <= b) continue;  // empty range
         const int slot = (b >= t0) ? 0 : 1;                      // tile holds the range's first / last segment
-        soff[k++] = ((int64_t)cc * P2_SLOTS + slot) * 128 * NP;
+        soff[k++] = ((int64_t)(cc * CL + crank) * P2_SLOTS + slot) * 128 * NP;
       }
     }
     ncov = k;
