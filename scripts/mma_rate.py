@@ -16,3 +16,8 @@ for kind, name in enumerate(["tf32 TS N128", "bf16 TS N128", "tf32 SS N128", "tf
     out = h.debug_pass(0, 140 + kind, A, B)
     ms = h.debug_pass_timed(0, 140 + kind, A, B, 5)
     print("%-14s %.1f cycles/MMA (CTA 0 clock64), %.3f ms per 8000 MMAs/SM" % (name, float(out[0, 0]), ms))
+for kind, name in enumerate(["DFMA", "DMMA m8n8k4"]):
+    out = h.debug_pass(0, 150 + kind, A, B)
+    out = h.debug_pass(0, 150 + kind, A, B)
+    cyc, fl = float(out[0, 0]), float(out[1, 0])
+    print("%-12s %.1f fp64 flop/cycle/SM (CTA 0, 512 threads)" % (name, fl / cyc))
