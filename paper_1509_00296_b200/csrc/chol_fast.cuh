@@ -93,16 +93,19 @@ chol_rows_kernel(const double* __restrict__ G, int l, double tol, double* __rest
 }
 
 // Q (rows x l) = Y R'^{-1}: q R' = y by forward substitution, one thread per
-// row, 32-column blocks with the block's running values in registers; the
-// already solved columns are re-read from Q (L1/L2) for the off-diagonal
-// block updates. R' (fp32 copy) and 1/R'_ii in shared memory (broadcast).
-template <int NBMAX>
+// row. The row is processed in NB blocks of 32 columns (fully unrolled); a
+// solved block is stored and re-read as one batch of loads when a later block
+// needs it (register pressure, occupancy). R' (fp32 copy, row-major,
+// zero padded) and 1/R'_ii are broadcast from shared memory (LDS.128 for the
+// off-diagonal block updates). Rows of R' with a zero diagonal are dropped
+// columns (q = 0).
+template <int NB>
 __global__ void __launch_bounds__(128)
 trsm_rows_kernel(const float* __restrict__ Y, int64_t rows, int64_t ldy, const double* __restrict__ Rp, int l,
                  float* __restrict__ Q, int64_t ldq) {
-  constexpr int LP = 32 * NBMAX;
+  constexpr int LP = 32 * NB;
   extern __shared__ float trs[];
-  float* R = trs;            // [LP][LP] row-major, zero padded
+  float* R = trs;             // [LP][LP]
   float* rin = trs + LP * LP;
   for (int idx = threadIdx.x; idx < LP * LP; idx += blockDim.x) {
     const int i = idx / LP, j = idx % LP;
@@ -115,31 +118,42 @@ trsm_rows_kernel(const float* __restrict__ Y, int64_t rows, int64_t ldy, const d
   __syncthreads();
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (row >= rows) return;
-  const int nb = (l + 31) >> 5;
-  for (int b = 0; b < nb; ++b) {
-    const int c0 = 32 * b;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
     float acc[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) acc[c] = (c0 + c < l) ? Y[row + (int64_t)(c0 + c) * ldy] : 0.f;
-    for (int k = 0; k < c0; ++k) {
-      const float qk = Q[row + (int64_t)k * ldq];
-      const float4* r4 = reinterpret_cast<const float4*>(R + k * LP + c0);
+    for (int c = 0; c < 32; ++c) acc[c] = (32 * b + c < l) ? Y[row + (int64_t)(32 * b + c) * ldy] : 0.f;
+#pragma unroll 1
+    for (int bp = 0; bp < b; ++bp) {
+      // the already solved block bp, re-read as one batch of independent loads
+      // (this thread wrote it; L1/L2 hits) instead of holding all q in registers
+      float qb[32];
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 rv = r4[c4];
-        acc[4 * c4 + 0] = fmaf(-qk, rv.x, acc[4 * c4 + 0]);
-        acc[4 * c4 + 1] = fmaf(-qk, rv.y, acc[4 * c4 + 1]);
-        acc[4 * c4 + 2] = fmaf(-qk, rv.z, acc[4 * c4 + 2]);
-        acc[4 * c4 + 3] = fmaf(-qk, rv.w, acc[4 * c4 + 3]);
+      for (int k = 0; k < 32; ++k) qb[k] = (32 * bp + k < l) ? Q[row + (int64_t)(32 * bp + k) * ldq] : 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float qk = qb[k];
+        const float4* r4 = reinterpret_cast<const float4*>(R + (32 * bp + k) * LP + 32 * b);
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 rv = r4[c4];
+          acc[4 * c4 + 0] = fmaf(-qk, rv.x, acc[4 * c4 + 0]);
+          acc[4 * c4 + 1] = fmaf(-qk, rv.y, acc[4 * c4 + 1]);
+          acc[4 * c4 + 2] = fmaf(-qk, rv.z, acc[4 * c4 + 2]);
+          acc[4 * c4 + 3] = fmaf(-qk, rv.w, acc[4 * c4 + 3]);
+        }
       }
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float q = acc[i] * rin[c0 + i];
-      if (c0 + i < l) Q[row + (int64_t)(c0 + i) * ldq] = q;
+      const float qi = acc[i] * rin[32 * b + i];
+      acc[i] = qi;
 #pragma unroll
-      for (int c = i + 1; c < 32; ++c) acc[c] = fmaf(-q, R[(c0 + i) * LP + c0 + c], acc[c]);
+      for (int c = i + 1; c < 32; ++c) acc[c] = fmaf(-qi, R[(32 * b + i) * LP + 32 * b + c], acc[c]);
     }
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (32 * b + c < l) Q[row + (int64_t)(32 * b + c) * ldq] = acc[c];
   }
 }
 

@@ -614,7 +614,7 @@ frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, 
 // final basis of the range finder (orth_final).
 template <int NB>
 frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float* Out) {
-  const size_t smem = (size_t)(32 * NB) * (32 * NB + 1) * sizeof(float);
+  const size_t smem = (size_t)(32 * NB) * (32 * NB + 1) * sizeof(float) + 16;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(trsm_rows_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -627,9 +627,10 @@ frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float*
 template <typename T>
 frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
   if constexpr (sizeof(T) == 4) {
-    if (h->fastchol) {  // R' by the register-resident Cholesky, Q1 = Y R'^{-1} by row-parallel TRSM
+    if (h->fastchol) {  // R' by the blocked Cholesky (no inverse), Q1 = Y R'^{-1} by row-parallel TRSM
       TRY(gram<T>(h, In, rows, rows, sharded));
-      chol_rows_kernel<<<1, CHR_THREADS, 0, h->st>>>(h->G, h->l, 1e-12, h->Rf, &h->dev->s, &h->dev->flags, nullptr);
+      orth_chol_kernel<float><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(
+          h->G, h->l, 1e-12, (float*)nullptr, &h->dev->s, &h->dev->flags, nullptr, nullptr, h->Rf);
       TRY(post_launch(h));
       if (h->l <= 32) return trsm_rows_nb<1>(h, (const float*)In, rows, (float*)Out);
       if (h->l <= 64) return trsm_rows_nb<2>(h, (const float*)In, rows, (float*)Out);
@@ -1134,8 +1135,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->p2cl = (e5 && e5[0] == '1') ? 1 : 2;
     const char* e3 = getenv("FRSVT_LOWDIN");
     h->lowdin = !(e3 && e3[0] == '0');
-    const char* e4 = getenv("FRSVT_FASTCHOL");  // experimental (slower so far): opt in with 1
-    h->fastchol = (e4 && e4[0] == '1');
+    const char* e4 = getenv("FRSVT_FASTCHOL");
+    h->fastchol = !(e4 && e4[0] == '0');
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||

@@ -33,7 +33,10 @@ template <typename Tq>
 __global__ void __launch_bounds__(OC_THREADS, 1)
 orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict__ T, int* __restrict__ s_out,
                  int* __restrict__ flags, unsigned long long* __restrict__ prof = nullptr,
-                 const int* __restrict__ skip = nullptr) {
+                 const int* __restrict__ skip = nullptr, double* __restrict__ Rout = nullptr) {
+  // Rout (nullable): stop after the factorisation and write R' = R diag(dsc)^{-1}
+  // (l x l row-major upper, fp64; dropped rows and diagonals 0) for the
+  // row-parallel TRSM apply Y R'^{-1} = Y diag(dsc) R^{-1}; T is not written.
   // skip (nullable): a device flag set when the Loewdin path already produced T
   if (skip && *skip) return;
   // prof (test hook, nullable): %globaltimer stamps at phase boundaries
@@ -164,6 +167,20 @@ orth_chol_kernel(const double* __restrict__ G, int l, double tol, Tq* __restrict
   }
 
   OC_STAMP(4);
+  if (Rout) {
+    for (int idx = tid; idx < l * l; idx += OC_THREADS) {
+      const int i = idx / l, j = idx % l;
+      double v = 0.0;
+      if (j >= i && keep[i] && dsc[j] > 0.0) v = S[(size_t)i * l + j] / dsc[j];
+      Rout[idx] = v;
+    }
+    if (tid == 0) {
+      int s = 0;
+      for (int i = 0; i < l; ++i) s += keep[i];
+      *s_out = s;
+    }
+    return;
+  }
   // T~ = R^{-1} on the kept set (dropped rows/columns are zero), by 32 x 32
   // blocks: (A) the diagonal blocks, one warp each, back substitution in
   // registers (lane = column); (B) block diagonals d = 1.. in parallel:
