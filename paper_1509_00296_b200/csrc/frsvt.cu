@@ -74,6 +74,9 @@ struct frsvt_handle {
   int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
   int p2cl;          // stream-K pass cluster size (1, or 2: B stages multicast to a CTA pair)
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
+  int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
+  unsigned int* tilecnt;  // per-tile arrival counters (zero between passes)
+  int ncnt;
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
   double* E2b;       // Loewdin workspace E^2 (l x l fp64)
   double* Rf;        // first-pass CholeskyQR factor R' (l x l row-major fp64)
@@ -377,10 +380,11 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
+  unsigned int* cnt = (h->infix && mtiles <= h->ncnt && !(dbg & 96)) ? h->tilecnt : nullptr;
   CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
-                        ldadd, h->skpart, rp_dev, dbg));
+                        ldadd, h->skpart, rp_dev, dbg, cnt));
   TRY(post_launch(h));
-  if (dbg & 96) return FRSVT_OK;
+  if ((dbg & 96) || cnt) return FRSVT_OK;
   // one block per (tile, 8-column group): enough independent loads in flight
   tc::tc_fixup_kernel<NP, CL><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
       Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
@@ -627,6 +631,13 @@ frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float*
 template <typename T>
 frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
   if constexpr (sizeof(T) == 4) {
+    if (h->fastchol == 2 || (h->fastchol == 3 && tc_small_ok(h, rows))) {
+      // Cholesky with explicit T, applied on tensor cores (tf32-level products
+      // as the SIMT fp32 apply: ~1e-6 of |Y||T|)
+      TRY(gram<T>(h, In, rows, rows, sharded));
+      TRY(chol<T>(h, (T*)h->T1));
+      return apply_fast<T>(h, In, rows, (const T*)h->T1, Out);
+    }
     if (h->fastchol) {  // R' by the blocked Cholesky (no inverse), Q1 = Y R'^{-1} by row-parallel TRSM
       TRY(gram<T>(h, In, rows, rows, sharded));
       orth_chol_kernel<float><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(
@@ -1021,7 +1032,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->tilecnt, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1129,14 +1140,23 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
+    const char* e7 = getenv("FRSVT_INFIX");
+    h->infix = !(e7 && e7[0] == '0');
+    h->ncnt = (int)cdiv(maxrows, 128) + 8;
+    if (cudaMalloc((void**)&h->tilecnt, sizeof(unsigned int) * h->ncnt) != cudaSuccess ||
+        cudaMemset(h->tilecnt, 0, sizeof(unsigned int) * h->ncnt) != cudaSuccess) {
+      cudaGetLastError();
+      free_handle(h);
+      return FRSVT_ENOMEM;
+    }
     const char* e6 = getenv("FRSVT_DMMA_GRAM");
     h->dmma_gram = !(e6 && e6[0] == '0');
     const char* e5 = getenv("FRSVT_P2CL");
     h->p2cl = (e5 && e5[0] == '1') ? 1 : 2;
     const char* e3 = getenv("FRSVT_LOWDIN");
     h->lowdin = !(e3 && e3[0] == '0');
-    const char* e4 = getenv("FRSVT_FASTCHOL");
-    h->fastchol = !(e4 && e4[0] == '0');
+    const char* e4 = getenv("FRSVT_FASTCHOL");  // 0: T + SIMT apply, 1: R + TRSM, 2/3: T + tensor apply
+    h->fastchol = e4 ? (e4[0] - '0') : 1;
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||

@@ -196,7 +196,12 @@ __global__ void __launch_bounds__(P2_THREADS, 1)
 tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
                 const __grid_constant__ CUtensorMap mapBl, int Mtot, int Ktot, int Nvalid, int nbrows,
                 float* __restrict__ out, int64_t ldo, const float* __restrict__ add, int64_t ldadd,
-                float* __restrict__ part, const int* __restrict__ rp_dev, int dbg) {
+                float* __restrict__ part, const int* __restrict__ rp_dev, int dbg,
+                unsigned int* __restrict__ tile_cnt) {
+  // tile_cnt (nullable, >= mtiles zeros): in-kernel stream-K fixup. The CTA
+  // that completes the last partial segment of a split tile sums all its
+  // partial slots in CTA order (deterministic), writes the tile and re-arms
+  // the counter; without it tc_fixup_kernel does this afterwards.
   // rp_dev (MODE_AX, range propagation): r = *rp_dev carried columns; only the
   // p = Nvalid - r fresh columns are multiplied (B holds them at [0, p), the
   // MMA runs with N = roundup16(p)) and land in out[:, r + c]; out[:, :r] is a
@@ -513,6 +518,60 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           float* p = part + ((int64_t)cta * P2_SLOTS + slot) * 128 * NP;
 #pragma unroll
           for (int j = 0; j < HALF; ++j) p[(int64_t)(col0 + j) * 128 + row] = sum[j];
+          if (tile_cnt) {
+            // covering work groups of this work tile, and whether this CTA is the last to finish
+            __shared__ int s_last;
+            __shared__ int s_c0, s_c1;
+            __threadfence();
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 flush warps
+            if (warp == 12 && lane == 0) {
+              const int64_t t0 = (int64_t)tile * nch, t1 = t0 + nch;
+              int c0 = (int)((t0 * G) / total);
+              while (c0 > 0 && p2_range_begin(total, G, c0) > t0) --c0;
+              while (p2_range_begin(total, G, c0 + 1) <= t0) ++c0;
+              int c1 = c0;
+              while (c1 + 1 < G && p2_range_begin(total, G, c1 + 1) < t1) ++c1;
+              int nc = 0;
+              for (int cc = c0; cc <= c1; ++cc) nc += (p2_range_begin(total, G, cc + 1) > p2_range_begin(total, G, cc));
+              const int atile = tile * CL + crank;
+              const unsigned int old = atomicAdd(&tile_cnt[atile], 1u);
+              s_last = (old + 1 == (unsigned int)nc) ? 1 : 0;
+              if (s_last) tile_cnt[atile] = 0u;  // re-arm for the next pass
+              s_c0 = c0;
+              s_c1 = c1;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (s_last) {
+              __threadfence();
+              const int gm = (tile * CL + crank) * 128 + row;
+              const int64_t t0 = (int64_t)tile * nch;
+              float* acc = sum;  // this CTA's own partial is re-read from its slot like the others
+#pragma unroll
+              for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
+              for (int cc = s_c0; cc <= s_c1; ++cc) {
+                const int64_t b = p2_range_begin(total, G, cc);
+                if (p2_range_begin(total, G, cc + 1) <= b) continue;
+                const int sl = (b >= t0) ? 0 : 1;
+                const float* q = part + ((int64_t)(cc * CL + crank) * P2_SLOTS + sl) * 128 * NP;
+#pragma unroll
+                for (int j = 0; j < HALF; ++j) acc[j] += __ldcg(q + (int64_t)(col0 + j) * 128 + row);
+              }
+              if (gm < Mtot) {
+#pragma unroll
+                for (int j = 0; j < HALF; ++j) {
+                  const int c = col0 + j;
+                  if (rp_dev) {
+                    if (c < nact) out[gm + (int64_t)(rsh + c) * ldo] = acc[j];
+                    if (c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+                  } else if (c < Nvalid) {
+                    float x = acc[j];
+                    if (add) x += add[gm + (int64_t)c * ldadd];
+                    out[gm + (int64_t)c * ldo] = x;
+                  }
+                }
+              }
+            }
+          }
         }
 #pragma unroll
         for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
