@@ -202,6 +202,19 @@ frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* 
  * boundaries. Synchronises. */
 frsvt_status frsvt_debug_chol(frsvt_handle* h, const double* G, void* T, int32_t* s, unsigned long long* stamps);
 
+/* Test hook: the one-barrier-per-column factor kernel (chol_inv.cuh) alone,
+ * fp32 handles. G: device, l x l fp64 Gram (column-major) of Y = [Q~ | Y_p]
+ * whose first r columns (0 <= r <= l, host) are taken as orthonormal
+ * (reading R11). T: device, l x l fp32
+ * (column-major, ld l) receives, for r = 0, T with Y T orthonormal; for r > 0
+ * the apply matrix Tp = [-G12 T22 ; T22] in its first p = l - r columns (the
+ * rest zero), Y Tp spanning the part of range(Y) orthogonal to Q~. *s (host,
+ * nullable) = r + kept fresh rank; stamps (device, nullable, >= 6 x u64) =
+ * %globaltimer at phase boundaries. EINVAL for a non-fp32 handle or r outside
+ * [0, l]. Synchronises. */
+frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, void* T, int32_t* s,
+                                  unsigned long long* stamps);
+
 /* Pass profiling: with enable != 0 every kernel that streams the m x n
  * operand is bracketed by CUDA events on the handle's stream (enabling resets
  * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,

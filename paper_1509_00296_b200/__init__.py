@@ -278,6 +278,20 @@ class Frsvt:
                                                         ctypes.c_void_p(st.data_ptr() if st is not None else 0)))
         return (T, s.value, st.cpu().numpy()) if stamps else (T, s.value)
 
+    def debug_chol_inv(self, G, r=0, stamps=False):
+        """Explicit CholeskyQR factor (chol_inv.cuh) of an l x l Gram whose first
+        r columns are orthonormal; returns (T fp32 l x l, s[, stamps ns])."""
+        l = self.l
+        dev = torch.device("cuda", torch.cuda.current_device())
+        G = G.to(device=dev, dtype=torch.float64).t().contiguous().t()
+        T = torch.empty((l, l), dtype=torch.float32, device=dev).t()
+        st = torch.zeros(6, dtype=torch.int64, device=dev) if stamps else None
+        s = ctypes.c_int32()
+        _check("frsvt_debug_chol_inv", lib.frsvt_debug_chol_inv(
+            self._h, ctypes.c_void_p(G.data_ptr()), int(r), ctypes.c_void_p(T.data_ptr()), ctypes.byref(s),
+            ctypes.c_void_p(st.data_ptr() if st is not None else 0)))
+        return (T, s.value, st.cpu().numpy()) if stamps else (T, s.value)
+
     def profile(self, enable=True):
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 

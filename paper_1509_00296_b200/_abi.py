@@ -15,7 +15,7 @@ SYMBOLS = [
     "frsvt_draw_omega", "frsvt_get_carry", "frsvt_set_carry", "frsvt_reset_carry",
     "frsvt_set_call_index", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
     "frsvt_kernel_launches", "frsvt_profile", "frsvt_profile_read", "frsvt_debug_pass",
-    "frsvt_debug_small_svd", "frsvt_debug_pass_timed", "frsvt_debug_chol",
+    "frsvt_debug_small_svd", "frsvt_debug_pass_timed", "frsvt_debug_chol", "frsvt_debug_chol_inv",
 ]
 
 
@@ -72,6 +72,7 @@ def load_library(path=LIB_PATH):
         "frsvt_debug_small_svd": (i32, [vp, i32, vp, vp, vp, vp, P(i32), i32, P(dbl)]),
         "frsvt_debug_pass_timed": (i32, [vp, i32, i32, vp, i64, vp, vp, i32, P(dbl)]),
         "frsvt_debug_chol": (i32, [vp, vp, vp, P(i32), vp]),
+        "frsvt_debug_chol_inv": (i32, [vp, vp, i32, vp, P(i32), vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

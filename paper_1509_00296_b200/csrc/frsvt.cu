@@ -19,6 +19,7 @@
 #include "orth_chol.cuh"
 #include "lowdin.cuh"
 #include "chol_fast.cuh"
+#include "chol_inv.cuh"
 #include "gram_dmma.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
@@ -80,7 +81,7 @@ struct frsvt_handle {
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
   double* E2b;       // Loewdin workspace E^2 (l x l fp64)
   double* Rf;        // first-pass CholeskyQR factor R' (l x l row-major fp64)
-  int fastchol;      // 1: chol_rows_kernel + trsm_rows_kernel (fp32 handles)
+  int fastchol;      // fp32 orth1: 4 chol_inv + tensor apply (default), 1 R + row TRSM, 2/3 T + tensor apply, 0 SIMT
   double *T2d, *Hd, *McD, *MpD;  // fp64 l x l: pending second CholeskyQR factor and fold scratch
   int t2_pending;    // 1: h->Q holds Q1 and the basis is Q1 T2d (T2d folded into G, Mc, Mp)
   int* lwd;          // device ints: [0] ok flag, [2..3] max|E| (u64)
@@ -365,9 +366,15 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
     attr_set = true;
   }
   const int mtiles = (int)cdiv(Mtot, 128);
-  const int64_t total = (int64_t)cdiv(mtiles, CL) * cdiv(Ktot, tc::BK);
+  const int64_t mgroups = cdiv(mtiles, CL);
+  const int64_t total = mgroups * cdiv(Ktot, tc::BK);
   const int Gmax = h->nsm / CL;
-  const int G = (int)(total < Gmax ? total : Gmax);  // work groups (clusters)
+  // small K (the l x l applies of the orthonormalisation): whole tiles per
+  // work group, no split tiles (dbg bit 8)
+  const bool talign = Ktot <= 8 * tc::BK && !(dbg & 96);
+  if (talign) dbg |= 256;
+  const int64_t units = talign ? mgroups : total;
+  const int G = (int)(units < Gmax ? units : Gmax);  // work groups (clusters)
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(G * CL));
   lc.blockDim = dim3(tc::P2_THREADS);
@@ -384,7 +391,7 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
   CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
                         ldadd, h->skpart, rp_dev, dbg, cnt));
   TRY(post_launch(h));
-  if ((dbg & 96) || cnt) return FRSVT_OK;
+  if ((dbg & 96) || cnt || talign) return FRSVT_OK;
   // one block per (tile, 8-column group): enough independent loads in flight
   tc::tc_fixup_kernel<NP, CL><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
       Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
@@ -410,7 +417,8 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
   const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
   const int64_t kx = cdiv(Ktot, tc::BK) * 2 * tc::BK;  // rows of the bf16 [b_l | b_h] operand
-  tc::split_tf32_bf16x2_kernel<<<grid1d(kx * h->l), 256, 0, h->st>>>(B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
+  tc::split_tf32_bf16x2_kernel<<<dim3((unsigned)cdiv(kx / 2, 256), (unsigned)h->l), 256, 0, h->st>>>(
+      B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
   TRY(post_launch(h));
   CUtensorMap mA, mBh, mBl;
   const uint32_t nb = h->p2cl == 2 ? 64u : (uint32_t)h->l;  // clustered: each CTA loads a 64-row half
@@ -506,7 +514,7 @@ template <> ncclDataType_t nccl_type<double>() { return ncclFloat64; }
 
 // G (l x l fp64) = Y^T Y over `rows` rows; summed over ranks if `sharded`.
 template <typename T>
-frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded) {
+frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded, const int* r_dev = nullptr) {
   const int l = h->l;
   if (h->dmma_gram) {  // fp64 tensor cores, upper 8x8 blocks only (gram_dmma.cuh)
     int S = (int)cdiv(rows, 256);
@@ -516,7 +524,7 @@ frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sh
     if (S < 1) S = 1;
     const int64_t rpc = cdiv(cdiv(rows, S), GD_ROWS) * GD_ROWS;
     S = (int)cdiv(rows, rpc);
-    gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd);
+    gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd, r_dev);
     TRY(post_launch(h));
     splitk_reduce_wide_kernel<double, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(h->partd, S, l,
                                                                                                      l, h->G, l);
@@ -628,9 +636,31 @@ frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float*
   return post_launch(h);
 }
 
+// CholeskyQR first pass with the explicit factor T of chol_inv_kernel (one
+// barrier per column, no triangular solve) applied by the stream-K tensor-core
+// pass. r_dev (range propagation, reading R11): In = [Q~ | Y_p]; only the
+// fresh block is factored and, in place (Out == In), Y_p <- (Y_p - Q~ Q~^T Y_p) T22.
+frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Out, bool sharded, const int* r_dev) {
+  const int l = h->l;
+  TRY(gram<float>(h, In, rows, rows, sharded, r_dev));
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(chol_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)chol_inv_smem_bytes()));
+    attr = true;
+  }
+  chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, l, r_dev, 1e-12, (float*)h->T1, l,
+                                                                          &h->dev->s, &h->dev->flags, nullptr);
+  TRY(post_launch(h));
+  // r_dev: in place (Out == In): only the fresh columns are written
+  return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev);
+}
+
 template <typename T>
 frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
   if constexpr (sizeof(T) == 4) {
+    if (h->fastchol == 4 && h->pass2 && tc_small_ok(h, rows))
+      return orth1_inv(h, (const float*)In, rows, (float*)Out, sharded, nullptr);
     if (h->fastchol == 2 || (h->fastchol == 3 && tc_small_ok(h, rows))) {
       // Cholesky with explicit T, applied on tensor cores (tf32-level products
       // as the SIMT fp32 apply: ~1e-6 of |Y||T|)
@@ -750,9 +780,19 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   const bool sh = h->cfg.nranks > 1;
   h->t2_pending = 0;
   if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh);
-  TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
+  // with range propagation on the tensor path the sketch basis is formed in
+  // place in Y: [Q~ | orth(Y_p - Q~ Q~^T Y_p)] (reading R11)
+  const T* Qcur = (const T*)h->Q;
+  bool rp_orth = false;
+  if constexpr (sizeof(T) == 4) rp_orth = rp_front && h->fastchol == 4 && h->pass2 && tc_small_ok(h, h->m);
+  if (rp_orth) {
+    if constexpr (sizeof(T) == 4) TRY(orth1_inv(h, (const float*)h->Y, h->m, (float*)h->Y, sh, &h->dev->r));
+    Qcur = (const T*)h->Y;
+  } else {
+    TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
+  }
   for (int it = 0; it < q; ++it) {
-    TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
+    TRY(gemm_AtQ<T>(h, A, lda, it == 0 ? Qcur : (const T*)h->Q, (T*)h->Z));
     TRY(orth1<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, false));
     TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr));
     if (it + 1 < q) TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
@@ -1156,7 +1196,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     const char* e3 = getenv("FRSVT_LOWDIN");
     h->lowdin = !(e3 && e3[0] == '0');
     const char* e4 = getenv("FRSVT_FASTCHOL");  // 0: T + SIMT apply, 1: R + TRSM, 2/3: T + tensor apply
-    h->fastchol = e4 ? (e4[0] - '0') : 1;
+    h->fastchol = e4 ? (e4[0] - '0') : 4;
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
@@ -1449,6 +1489,23 @@ frsvt_status frsvt_debug_chol(frsvt_handle* h, const double* G, void* T, int32_t
   else
     orth_chol_kernel<double><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(h->G, h->l, tol, (double*)T,
                                                                                  &h->dev->s, &h->dev->flags, stamps);
+  TRY(post_launch(h));
+  CK(cudaStreamSynchronize(h->st));
+  if (s) CK(cudaMemcpy(s, &h->dev->s, sizeof(int), cudaMemcpyDeviceToHost));
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, void* T, int32_t* s,
+                                  unsigned long long* stamps) {
+  if (!h || !G || !T || h->esz != 4 || r < 0 || r > h->l) return FRSVT_EINVAL;
+  CK(cudaMemcpyAsync(h->G, G, sizeof(double) * h->l * h->l, cudaMemcpyDeviceToDevice, h->st));
+  int* rd = h->lwd + 4;  // scratch int (lwd[0..3]: Loewdin flags)
+  CK(cudaMemcpyAsync(rd, &r, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  CK(cudaFuncSetAttribute(chol_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)chol_inv_smem_bytes()));
+  chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, h->l, rd, 1e-12, (float*)T, h->l,
+                                                                          &h->dev->s, &h->dev->flags, nullptr,
+                                                                          stamps);
   TRY(post_launch(h));
   CK(cudaStreamSynchronize(h->st));
   if (s) CK(cudaMemcpy(s, &h->dev->s, sizeof(int), cudaMemcpyDeviceToHost));

@@ -27,11 +27,15 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
 template <typename Tin>
 __global__ void __launch_bounds__(GD_THREADS)
 gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, int64_t rows_per_cta,
-                 double* __restrict__ part) {
+                 double* __restrict__ part, const int* __restrict__ r_dev = nullptr) {
+  // r_dev (nullable, range propagation): only the 8 x 8 blocks whose column
+  // block reaches the fresh columns [r, l) are formed (G12 and G22, the
+  // entries chol_inv_kernel reads); the rest of the partial is left stale.
   __shared__ double sY[GD_ROWS * GD_LD];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb8 = (l + 7) >> 3;
   const int nblk = nb8 * (nb8 + 1) / 2;
+  const int jb0 = r_dev ? (min(max(*r_dev, 0), l) >> 3) : 0;
   // this warp's blocks: q = warp + 8 t, (bi <= bj) in row-major upper order
   int bi[GD_MAXB], bj[GD_MAXB];
   double acc0[GD_MAXB], acc1[GD_MAXB];
@@ -45,6 +49,7 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
       }
       bi[t] = i;
       bj[t] = i + q;
+      if (bj[t] < jb0) bi[t] = bj[t] = -1;
     } else {
       bi[t] = -1;
       bj[t] = -1;

@@ -240,7 +240,11 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int64_t total = (int64_t)mgroups * nch;
   const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   const int G = gridDim.x / CL, cta = blockIdx.x, cgrp = blockIdx.x / CL;
-  const int64_t g0 = p2_range_begin(total, G, cgrp), g1 = p2_range_begin(total, G, cgrp + 1);
+  // dbg bit 8 (small K): ranges of whole work tiles, so no tile is split and
+  // no partial slots or fixup are needed
+  const bool talign = (dbg & 256) != 0;
+  const int64_t g0 = talign ? ((int64_t)mgroups * cgrp / G) * nch : p2_range_begin(total, G, cgrp);
+  const int64_t g1 = talign ? ((int64_t)mgroups * (cgrp + 1) / G) * nch : p2_range_begin(total, G, cgrp + 1);
   const int nloc = (int)(g1 - g0);
   // expected TMA bytes per B stage (CL = 1: boxes of nbrows rows; CL = 2: both
   // CTAs' 64-row halves, out-of-bounds rows zero-filled and counted)
@@ -504,7 +508,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
               const int c = col0 + j;
               if (rp_dev) {
                 if (c < nact) out[gm + (int64_t)(rsh + c) * ldo] = sum[j];
-                if (c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+                if (add && c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
               } else if (c < Nvalid) {
                 float x = sum[j];
                 if (add) x += add[gm + (int64_t)c * ldadd];
@@ -562,7 +566,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                   const int c = col0 + j;
                   if (rp_dev) {
                     if (c < nact) out[gm + (int64_t)(rsh + c) * ldo] = acc[j];
-                    if (c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+                    if (add && c < rsh) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
                   } else if (c < Nvalid) {
                     float x = acc[j];
                     if (add) x += add[gm + (int64_t)c * ldadd];
@@ -639,8 +643,8 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
     const int row = idx & 127, c = cb + (idx >> 7);
     const int gm = tile * 128 + row;
     if (gm >= Mtot) continue;
-    if (rp_dev && c < rsh) {  // carried column
-      out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+    if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
+      if (add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
       continue;
     }
     const int ca = c - rsh;  // accumulator column
@@ -654,30 +658,24 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
 // B operand split: Bh = rna_tf32(x) (fp32, rows x cols, ld ldh) and Bx (bf16,
 // (2 * roundup32(rows)) x cols, ld ldx): for K chunk c, Bx rows 64c + j hold
 // bf16(x - Bh) at K = 32c + j (j < 32) and bf16(Bh) at K = 32c + j - 32
-// (j >= 32), zero past `rows`. One thread per Bx element.
-__global__ void split_tf32_bf16x2_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx_in,
-                                         float* __restrict__ Bh, int64_t ldh, __nv_bfloat16* __restrict__ Bx,
-                                         int64_t ldx) {
-  const int64_t kp = ((rows + 31) / 32) * 64;
-  const int64_t total = kp * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r2 = idx % kp, j = idx / kp;
-    const int64_t c = r2 >> 6, w = r2 & 63;
-    const int64_t k = 32 * c + (w & 31);
-    float v = 0.f;
-    if (k < rows) {
-      const float x = X[k + j * ldx_in];
-      const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-      if (w < 32) {
-        v = x - h;
-        Bh[k + j * ldh] = h;
-      } else {
-        v = h;
-      }
-    }
-    Bx[r2 + j * ldx] = __float2bfloat16_rn(v);
+// (j >= 32), zero past `rows`. One thread per (row, column), writing both halves.
+__global__ void __launch_bounds__(256) split_tf32_bf16x2_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
+                                                                  int64_t ldx_in, float* __restrict__ Bh, int64_t ldh,
+                                                                  __nv_bfloat16* __restrict__ Bx, int64_t ldx) {
+  // grid (chunks of 256 rows, cols): thread = one row k of column j
+  const int j = blockIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t kpad = ((rows + 31) / 32) * 32;
+  if (k >= kpad) return;
+  float x = 0.f, h = 0.f;
+  if (k < rows) {
+    x = X[k + j * ldx_in];
+    h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+    Bh[k + j * ldh] = h;
   }
+  const int64_t base = (k >> 5) * 64 + (k & 31) + j * ldx;
+  Bx[base] = __float2bfloat16_rn(x - h);
+  Bx[base + 32] = __float2bfloat16_rn(h);
 }
 
 }  // namespace tc
