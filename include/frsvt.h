@@ -210,7 +210,7 @@ frsvt_status frsvt_debug_chol(frsvt_handle* h, const double* G, void* T, int32_t
  * the apply matrix Tp = [-G12 T22 ; T22] in its first p = l - r columns (the
  * rest zero), Y Tp spanning the part of range(Y) orthogonal to Q~. *s (host,
  * nullable) = r + kept fresh rank; stamps (device, nullable, >= 6 x u64) =
- * %globaltimer at phase boundaries. EINVAL for a non-fp32 handle or r outside
+ * %globaltimer at the phase boundaries. EINVAL for a non-fp32 handle or r outside
  * [0, l]. Synchronises. */
 frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, void* T, int32_t* s,
                                   unsigned long long* stamps);

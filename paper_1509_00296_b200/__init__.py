@@ -285,7 +285,7 @@ class Frsvt:
         dev = torch.device("cuda", torch.cuda.current_device())
         G = G.to(device=dev, dtype=torch.float64).t().contiguous().t()
         T = torch.empty((l, l), dtype=torch.float32, device=dev).t()
-        st = torch.zeros(6, dtype=torch.int64, device=dev) if stamps else None
+        st = torch.zeros(8, dtype=torch.int64, device=dev) if stamps else None
         s = ctypes.c_int32()
         _check("frsvt_debug_chol_inv", lib.frsvt_debug_chol_inv(
             self._h, ctypes.c_void_p(G.data_ptr()), int(r), ctypes.c_void_p(T.data_ptr()), ctypes.byref(s),

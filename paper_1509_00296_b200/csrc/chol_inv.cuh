@@ -1,5 +1,5 @@
 // CholeskyQR factor as an explicit triangular T (Y T has orthonormal columns),
-// one CTA of 1024 threads, one block barrier per column.
+// one CTA of 256 threads, one block barrier per column.
 //
 // Right-looking elimination of the equilibrated Gram S = D G D (D = diag(dsc),
 // dsc_i = G_ii^{-1/2}) with the inverse of the unit lower factor accumulated
@@ -32,41 +32,15 @@
 namespace frsvt {
 
 constexpr int CI_THREADS = 1024;
+#ifndef CI_PROF
+#define CI_PROF 0  // phase stamps (the test hook's `stamps`): build with -DCI_PROF=1
+#endif
 constexpr int CI_LD = FRSVT_LMAX;  // row stride (doubles) of the p x p work matrix
 
 __host__ __device__ constexpr size_t chol_inv_smem_bytes() {
-  // M (LMAX x CI_LD) + G12 (<= (LMAX/2)^2 when r, p > 0) + dsc + sd + 32 pivot rows + 32 pivot
-  // inverses + LMAX row barriers
-  return ((size_t)FRSVT_LMAX * CI_LD + (size_t)(FRSVT_LMAX / 2) * (FRSVT_LMAX / 2) + 2 * FRSVT_LMAX +
-          32 * (size_t)FRSVT_LMAX + 32 + FRSVT_LMAX) *
+  // M (LMAX x CI_LD) + G12 (<= (LMAX/2)^2 when r, p > 0) + dsc + sd + 2 pivot rows + 2 pivot inverses
+  return ((size_t)FRSVT_LMAX * CI_LD + (size_t)(FRSVT_LMAX / 2) * (FRSVT_LMAX / 2) + 4 * FRSVT_LMAX + 2) *
          sizeof(double);
-}
-
-__device__ __forceinline__ void ci_bar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
-}
-__device__ __forceinline__ void ci_bar_arrive(uint64_t* bar) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.release.cta.shared.b64 st, [%0];\n}" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-__device__ __forceinline__ void ci_bar_wait0(uint64_t* bar) {  // phase 0 completion (each barrier is used once)
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], 0;\nselp.b32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(a)
-        : "memory");
-  } while (!ok);
-}
-// 1 / d for d in (tol, ~1]: fp32 reciprocal + two Newton steps (~1 ulp)
-__device__ __forceinline__ double ci_rcp(double d) {
-  double r = (double)__frcp_rn((float)d);
-  r = fma(r, fma(-d, r, 1.0), r);
-  r = fma(r, fma(-d, r, 1.0), r);
-  return r;
 }
 
 // Storage during the elimination (before step k), M = the p x p work matrix:
@@ -77,13 +51,12 @@ __device__ __forceinline__ double ci_rcp(double d) {
 //   M_ab -= u_a M_kb   (b != k: Schur update for b > k, W update for b < k)
 //   M_ak  = -u_a       (W_ak; written as M_ak - u_a (S_kk + 1), since M_ak = S_ak = S_ka)
 // Thread (warp w, lane L) keeps the 4 x 4 entries (w + 32 i, L + 32 j) in
-// registers. Step k needs only row k, so there is no block barrier: the owner
-// warp of row k + 1 updates that row first in step k, publishes it (and
-// 1 / S_{k+1,k+1}) to ring slot (k + 1) mod 32 and arrives on the row's
-// one-shot mbarrier; every warp waits on row k's barrier before step k. A
-// slot is rewritten 32 rows later by the same warp, which by then waited on
-// rows published by all 31 other warps after their step k: no reader of row k
-// is left.
+// registers. After step k's update the owner warp of row k + 1 publishes
+// that row (and 1 / S_{k+1,k+1}) to a double-buffered shared row; one block
+// barrier per pivot. (Measured on B200, l = 120: ~600 ns per pivot,
+// latency-bound. Row mbarriers instead of the block barrier, the owner's row
+// updated first, or 8 warps with 16 rows each were all slower: the extra
+// live registers spill at the 64-register limit of 1024 threads.)
 template <typename Tq>
 __global__ void __launch_bounds__(CI_THREADS, 1)
 chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_dev, double tol, Tq* __restrict__ T,
@@ -93,7 +66,7 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   // prof (test hook, nullable): %globaltimer at phase boundaries
 #define CI_STAMP(q)                                          \
   do {                                                       \
-    if (prof && threadIdx.x == 0) {                          \
+    if (CI_PROF && prof && threadIdx.x == 0) {               \
       unsigned long long t_;                                 \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
       prof[q] = t_;                                          \
@@ -105,9 +78,8 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   double* X = M + (size_t)FRSVT_LMAX * CI_LD;    // G12, r x p row-major (X[c * p + i])
   double* dsc = X + (FRSVT_LMAX / 2) * (FRSVT_LMAX / 2);
   double* sd = dsc + FRSVT_LMAX;
-  double* rowbuf = sd + FRSVT_LMAX;              // 32 x LMAX ring of pivot rows
-  double* invbuf = rowbuf + 32 * FRSVT_LMAX;     // 32 pivot inverses
-  uint64_t* rbar = reinterpret_cast<uint64_t*>(invbuf + 32);  // LMAX one-shot row barriers
+  double* rowbuf = sd + FRSVT_LMAX;              // 2 x LMAX pivot rows
+  double* invbuf = rowbuf + 2 * FRSVT_LMAX;      // 2 pivot inverses
   const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
   const int r = r_dev ? min(max(*r_dev, 0), l) : 0;
   const int p = l - r;
@@ -137,6 +109,11 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
     }
   }
   __syncthreads();
+  CI_STAMP(2);
+  // (3) elimination: thread (warp w, lane L) holds the 4 x 4 entries
+  // (w + 32 i, L + 32 j) in registers; after the update the owner warp of row
+  // k + 1 publishes it with 1 / S_{k+1,k+1} (double-buffered); one block
+  // barrier per pivot
   double m[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -145,66 +122,59 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
       const int a = w + 32 * i, b = L + 32 * j;
       m[i][j] = (a < p && b < p) ? M[a * CI_LD + b] : 0.0;
     }
-  for (int i = tid; i < FRSVT_LMAX; i += CI_THREADS) ci_bar_init(&rbar[i]);
-  __syncthreads();
-  if (w == 0 && p > 0) {  // row 0
+  if (w == 0) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) rowbuf[L + 32 * j] = m[0][j];
-    if (L == 0) invbuf[0] = m[0][0] > tol ? ci_rcp(m[0][0]) : 0.0;
-    __syncwarp();
-    if (L == 0) ci_bar_arrive(&rbar[0]);
   }
-
-  CI_STAMP(2);
-  // (3) elimination
+  if (tid == 0) invbuf[0] = (p > 0 && m[0][0] > tol) ? 1.0 / m[0][0] : 0.0;
+  __syncthreads();
   for (int k = 0; k < p; ++k) {
-    ci_bar_wait0(&rbar[k]);
-    const double* rk = rowbuf + (k & 31) * FRSVT_LMAX;
-    const double inv = invbuf[k & 31];
+    const double* rk = rowbuf + (k & 1) * FRSVT_LMAX;
+    const double inv = invbuf[k & 1];
     const double d = rk[k];
-    double v[4], u[4];
+    if (inv != 0.0) {
+      double v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int b = L + 32 * j;
-      v[j] = (b == k) ? d + 1.0 : rk[b];
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int a = w + 32 * i;
-      u[i] = (a > k && a < p) ? rk[a] * inv : 0.0;
-    }
-    const int k1 = k + 1;
-    const bool owner = k1 < p && w == (k1 & 31);
-    const int i1 = k1 >> 5;
-    // row i is updated when active; the owner's row k + 1 first, then published
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = 0; j < 4; ++j) {
+        const int b = L + 32 * j;
+        v[j] = (b == k) ? d + 1.0 : rk[b];  // column k: M_ak - u_a (S_kk + 1) = -u_a
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int a = w + 32 * i;
-        const bool first = owner && i == i1;
-        if (a > k && a < p && (pass == 0) == first) {
-          if (inv != 0.0) {
+        if (a > k && a < p) {
+          const double u = rk[a] * inv;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) m[i][j] = fma(-u[i], v[j], m[i][j]);
-          } else {  // dropped pivot: no elimination, W_ak = 0
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (L + 32 * j == k) m[i][j] = 0.0;
-          }
+          for (int j = 0; j < 4; ++j) m[i][j] = fma(-u, v[j], m[i][j]);
         }
-        if (pass == 0 && first) {
-          double* rn = rowbuf + (k1 & 31) * FRSVT_LMAX;
+      }
+    } else {  // dropped pivot: no elimination, W_ak = 0
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            rn[L + 32 * j] = m[i][j];
-            if (j == i1 && L == (k1 & 31)) invbuf[k1 & 31] = m[i][j] > tol ? ci_rcp(m[i][j]) : 0.0;
-          }
-          __syncwarp();
-          if (L == 0) ci_bar_arrive(&rbar[k1]);
+      for (int i = 0; i < 4; ++i) {
+        const int a = w + 32 * i;
+        if (a > k && a < p) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (L + 32 * j == k) m[i][j] = 0.0;
         }
       }
     }
+    const int k1 = k + 1;
+    if (k1 < p && w == (k1 & 31)) {  // publish row k + 1 and its pivot inverse
+      double* rn = rowbuf + (k1 & 1) * FRSVT_LMAX;
+      const int i1 = k1 >> 5;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i == i1) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            rn[L + 32 * j] = m[i][j];
+            if (j == i1 && L == (k1 & 31)) invbuf[k1 & 1] = m[i][j] > tol ? 1.0 / m[i][j] : 0.0;
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)

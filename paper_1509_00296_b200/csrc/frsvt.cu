@@ -76,6 +76,7 @@ struct frsvt_handle {
   int p2cl;          // stream-K pass cluster size (1, or 2: B stages multicast to a CTA pair)
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
   int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
+  int ci_sync;       // chol_inv_kernel synchronisation mode (FRSVT_CI_SYNC)
   unsigned int* tilecnt;  // per-tile arrival counters (zero between passes)
   int ncnt;
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
@@ -1180,6 +1181,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
+    const char* e8 = getenv("FRSVT_CI_SYNC");
+    h->ci_sync = e8 ? (e8[0] - '0') : 0;
     const char* e7 = getenv("FRSVT_INFIX");
     h->infix = !(e7 && e7[0] == '0');
     h->ncnt = (int)cdiv(maxrows, 128) + 8;

@@ -28,5 +28,6 @@ for ev in prof.events():
         print("%8.1f us  %s" % (ev.device_time_total, ev.name[:80]))
 for r in (0, 100, 60):
     T, s, st = h.debug_chol_inv(G, r, stamps=True)
-    d = np.diff(st.astype(np.float64)) / 1e3
-    print("r %3d  load %.1f | schur %.1f | elimination %.1f | T22 %.1f | store %.1f us" % ((r,) + tuple(d)))
+    d = np.diff(st[:6].astype(np.float64)) / 1e3
+    print("r %3d  load %.1f | schur %.1f | elimination %.1f | T22 %.1f | store %.1f us (%.0f ns per pivot)"
+          % ((r,) + tuple(d) + (d[2] * 1e3 / (l - r),)))
