@@ -37,9 +37,9 @@
 //               swizzle), 3-deep ring released by the MMA
 //   warp 1      MMA issuer (one thread); A operands from TMEM, B from smem
 //   warp 2      TMEM allocator
-//   warps 4..11 converters (two per TMEM lane quarter, 16 K values each):
-//               A chunk -> a_h, a_l (tf32) and bf16(a_h) pairs -> TMEM ring
-//               (thread = TMEM lane = M row)
+//   warps 4..11 converters, two groups of four (one warp per TMEM lane
+//               quarter) on alternate chunks: A chunk -> a_h (tf32) and bf16
+//               [a_h | a_l] pairs -> TMEM ring (thread = TMEM lane = M row)
 //   warps 12..19 flush: double-buffered TMEM accumulator pieces (<= SEG
 //               chunks, never across a tile) -> fp32 registers -> output
 #pragma once
@@ -254,14 +254,14 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < P2_ASTAGES; ++s) {
       mbar_init(&fulla[s], 1);
-      mbar_init(&emptya[s], 8);
+      mbar_init(&emptya[s], 4);
     }
     for (int s = 0; s < P2_BSTAGES; ++s) {
       mbar_init(&fullb[s], 1);
       mbar_init(&emptyb[s], CL);
     }
     for (int t = 0; t < P2_TSTAGES; ++t) {
-      mbar_init(&tfull[t], 8);
+      mbar_init(&tfull[t], 4);
       mbar_init(&tempty[t], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -402,11 +402,14 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     }
   } else if (warp >= 4 && warp < 12) {
     // converters: A chunk in shared memory -> a_h, a_l, bf16(a_h) -> TMEM ring.
-    // Two warps per TMEM lane quarter, each converting 16 of the chunk's 32 K.
-    const int wq = warp & 3, kh = (warp - 4) >> 2;
+    // Two groups of four warps (one per TMEM lane quarter) take alternate
+    // chunks, each warp converting all 32 K of its 32 rows, so two chunks
+    // are in conversion at once (the load -> convert -> tcgen05.st -> wait
+    // chain of one chunk overlaps the other's).
+    const int wq = warp & 3, grp = (warp - 4) >> 2;
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    for (int i = 0; i < nloc; ++i) {
+    for (int i = grp; i < nloc; i += 2) {
       const int s = i % P2_ASTAGES;
       const uint32_t ph = (i / P2_ASTAGES) & 1;
       const int t = i % P2_TSTAGES;
@@ -422,44 +425,41 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         continue;
       }
       const uint32_t a_s = smem_u32(sA + s * A_BYTES);
-      uint32_t hi[16], lo[16], hb[8], lb[8];
+      uint32_t x[32], hb[16], lb[16];
       if (MODE == MODE_AX) {
         // box {128 rows, 32 cols}, no swizzle: (row, k) at (k*128 + row)*4
 #pragma unroll
-        for (int k = 0; k < 16; ++k) hi[k] = lds_u32(a_s + (uint32_t)(((16 * kh + k) * 128 + row) * 4));
+        for (int k = 0; k < 32; ++k) x[k] = lds_u32(a_s + (uint32_t)((k * 128 + row) * 4));
       } else {
         // box {32 rows (K), 128 cols (M)}, 128B swizzle: (j, k) at j*128 + ((k/4 ^ j%8) * 16) + (k%4)*4
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int cc = 4 * kh + c;
-          lds_u32x4(a_s + (uint32_t)(row * 128 + ((cc ^ (row & 7)) * 16)), hi[4 * c], hi[4 * c + 1], hi[4 * c + 2],
-                    hi[4 * c + 3]);
-        }
+        for (int c = 0; c < 8; ++c)
+          lds_u32x4(a_s + (uint32_t)(row * 128 + ((c ^ (row & 7)) * 16)), x[4 * c], x[4 * c + 1], x[4 * c + 2],
+                    x[4 * c + 3]);
       }
       // the A stage is free once its values are in registers
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptya[s]);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const uint32_t x = hi[k];
-        const uint32_t h = (x + 0x1000u) & 0xFFFFE000u;  // round to nearest tf32, ties away (finite x)
-        hi[k] = h;
-        lo[k] = __float_as_uint(__uint_as_float(x) - __uint_as_float(h));
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const __nv_bfloat162 p = __floats2bfloat162_rn(__uint_as_float(hi[2 * k]), __uint_as_float(hi[2 * k + 1]));
-        hb[k] = *reinterpret_cast<const uint32_t*>(&p);
-        const __nv_bfloat162 q = __floats2bfloat162_rn(__uint_as_float(lo[2 * k]), __uint_as_float(lo[2 * k + 1]));
-        lb[k] = *reinterpret_cast<const uint32_t*>(&q);
+        const uint32_t x0 = x[2 * k], x1 = x[2 * k + 1];
+        const uint32_t h0 = (x0 + 0x1000u) & 0xFFFFE000u, h1 = (x1 + 0x1000u) & 0xFFFFE000u;  // rna tf32
+        const __nv_bfloat162 hp = __floats2bfloat162_rn(__uint_as_float(h0), __uint_as_float(h1));
+        const __nv_bfloat162 lp = __floats2bfloat162_rn(__uint_as_float(x0) - __uint_as_float(h0),
+                                                        __uint_as_float(x1) - __uint_as_float(h1));
+        hb[k] = *reinterpret_cast<const uint32_t*>(&hp);
+        lb[k] = *reinterpret_cast<const uint32_t*>(&lp);
+        x[2 * k] = h0;
+        x[2 * k + 1] = h1;
       }
       mbar_wait(&tempty[t], tph ^ 1);
       if (warp == 4 && lane == 0) p2_stamp(dbg, out, 2, i, nloc);
       // stage layout: [0, 32) a_h tf32; [32, 48) bf16 a_h pairs (K' 0..31); [48, 64) bf16 a_l pairs (K' 32..63)
       const uint32_t ta = t_a + t * 64 + lane_off;
-      tmem_st16(ta + 16 * kh, hi);
-      tmem_st8(ta + 32 + 8 * kh, hb);
-      tmem_st8(ta + 48 + 8 * kh, lb);
+      tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(&x[0]));
+      tmem_st16(ta + 16, *reinterpret_cast<const uint32_t(*)[16]>(&x[16]));
+      tmem_st16(ta + 32, hb);
+      tmem_st16(ta + 48, lb);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
