@@ -24,6 +24,7 @@
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
 #include "tc_pass2.cuh"
+#include "tc_compose2.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -76,7 +77,7 @@ struct frsvt_handle {
   int p2cl;          // stream-K pass cluster size (1, or 2: B stages multicast to a CTA pair)
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
   int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
-  int ci_sync;       // chol_inv_kernel synchronisation mode (FRSVT_CI_SYNC)
+  int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
   unsigned int* tilecnt;  // per-tile arrival counters (zero between passes)
   int ncnt;
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
@@ -483,6 +484,31 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   if (sp > ntiles) sp = ntiles;
   if (sp < 1) sp = 1;
   dim3 grid((unsigned)(nfull + rem * sp));
+  if (h->cmp2 && epi != tc::EPI_STORE) {
+    CUtensorMap mD, mA, mE;
+    if (!make_map(&mD, D, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !make_map(&mE, E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !make_map(&mA, epi == tc::EPI_ALM ? A : E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return FRSVT_ECUDA;
+    const size_t smem2 = tc::Compose2Smem::total();
+    static bool attr2[3] = {false, false, false};
+#define FRSVT_LAUNCH_CMP2(EPIV)                                                                                 \
+  do {                                                                                                          \
+    if (!attr2[EPIV]) {                                                                                         \
+      CK(cudaFuncSetAttribute(tc::tc_compose2_kernel<EPIV>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                              (int)smem2));                                                                     \
+      attr2[EPIV] = true;                                                                                       \
+    }                                                                                                           \
+    tc::tc_compose2_kernel<EPIV><<<grid, tc::CMP_THREADS, smem2, h->st>>>(                                      \
+        mQh, mQl, mWh, mWl, mD, mA, mE, (int)h->m, (int)h->n, &h->dev->r, nfull, sp, X, ldx, A, E, ld,        \
+        h->dev->mu, rho, lambda, h->redpart);                                                                   \
+  } while (0)
+    if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP2(tc::EPI_ALM);
+    else FRSVT_LAUNCH_CMP2(tc::EPI_FINAL);
+#undef FRSVT_LAUNCH_CMP2
+    if (nparts) *nparts = (int)grid.x;
+    return post_launch(h);
+  }
   const size_t smem = tc::ComposeSmem::total();
   static bool attr[3] = {false, false, false};
 #define FRSVT_LAUNCH_CMP(EPIV)                                                                                  \
@@ -1181,8 +1207,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
-    const char* e8 = getenv("FRSVT_CI_SYNC");
-    h->ci_sync = e8 ? (e8[0] - '0') : 0;
+    const char* e8 = getenv("FRSVT_CMP2");
+    h->cmp2 = !(e8 && e8[0] == '0');
     const char* e7 = getenv("FRSVT_INFIX");
     h->infix = !(e7 && e7[0] == '0');
     h->ncnt = (int)cdiv(maxrows, 128) + 8;
