@@ -41,7 +41,7 @@ using namespace frsvt;
 namespace {
 
 struct DevState {
-  int s, r, flags, sweeps, have_prev, s2, pad1, pad2;
+  int s, r, flags, sweeps, have_prev, s2, fs_done, pad2;  // fs_done: next sketch formed by compose2
   double mu[2];        // mu_k, mu_bar
   double tau;
   double scal[4];      // 1/J, ||D||_2
@@ -78,6 +78,11 @@ struct frsvt_handle {
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
   int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
   int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
+  int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_FS)
+  bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
+  float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
+  float* OmT;        // Omega^T, n x 24 (the fused sketch's TMA operand)
+  size_t fspart_ctas;
   unsigned int* tilecnt;  // per-tile arrival counters (zero between passes)
   int ncnt;
   int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
@@ -359,7 +364,7 @@ frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q
 template <int MODE, int NP, int CL>
 frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
-                          const int* rp_dev) {
+                          const int* rp_dev, const int* skip_dev = nullptr) {
   const size_t smem = tc::Pass2Smem::total(CL > 1 ? 128 : h->l);
   static bool attr_set = false;
   if (!attr_set) {
@@ -391,7 +396,7 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
   lc.numAttrs = 1;
   unsigned int* cnt = (h->infix && mtiles <= h->ncnt && !(dbg & 96)) ? h->tilecnt : nullptr;
   CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
-                        ldadd, h->skpart, rp_dev, dbg, cnt));
+                        ldadd, h->skpart, rp_dev, dbg, cnt, skip_dev));
   TRY(post_launch(h));
   if ((dbg & 96) || cnt || talign) return FRSVT_OK;
   // one block per (tile, 8-column group): enough independent loads in flight
@@ -403,10 +408,10 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
 template <int MODE, int NP>
 frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
-                          const int* rp_dev = nullptr) {
+                          const int* rp_dev = nullptr, const int* skip_dev = nullptr) {
   if (h->p2cl == 2)
-    return launch_p2_cl<MODE, NP, 2>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev);
-  return launch_p2_cl<MODE, NP, 1>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+    return launch_p2_cl<MODE, NP, 2>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
+  return launch_p2_cl<MODE, NP, 1>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
 }
 
 // out (Mtot x l) = op(A) * B, B (Ktot x l, ld ldb) the small operand:
@@ -414,7 +419,7 @@ frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
 template <int MODE>
 frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
                       int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
-                      const int* rp_dev = nullptr) {
+                      const int* rp_dev = nullptr, const int* skip_dev = nullptr) {
   float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
   __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
   const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
@@ -439,10 +444,10 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   if (!ok) return FRSVT_ECUDA;
   const int np = tc_np(h->l);
   if (np == 32)
-    return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+    return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
   if (np == 64)
-    return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
-  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev);
+    return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
+  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
 }
 
 // tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows) matrix
@@ -453,7 +458,7 @@ bool tc_small_ok(const frsvt_handle* h, int64_t rows) {
 // X = Q~ Wt^T fused with its consumer (tc::EPI_*) on tensor cores. Returns the
 // number of residual partials written to h->redpart.
 frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const float* D, float* A, float* E,
-                        int64_t ld, double rho, double lambda, int* nparts) {
+                        int64_t ld, double rho, double lambda, int* nparts, bool fs_next = false) {
   const int Kp = h->Kp;
   {
     dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
@@ -490,24 +495,41 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
         !make_map(&mE, E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mA, epi == tc::EPI_ALM ? A : E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
       return FRSVT_ECUDA;
+    // fused next sketch (fs): Omega of the next call (already drawn into h->Om)
+    const bool fs = fs_next && epi == tc::EPI_ALM && grid.x <= h->fspart_ctas;
+    CUtensorMap mOm = mD;
+    if (fs) {
+      tc::omega_t24_kernel<<<grid1d(h->n * tc::FS_PMAX), 256, 0, h->st>>>((const float*)h->Om, h->n, h->l, h->OmT);
+      TRY(post_launch(h));
+      if (!make_map(&mOm, h->OmT, tc::FS_PMAX, h->n, tc::FS_PMAX, tc::FS_PMAX, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return FRSVT_ECUDA;
+    }
     const size_t smem2 = tc::Compose2Smem::total();
-    static bool attr2[3] = {false, false, false};
-#define FRSVT_LAUNCH_CMP2(EPIV)                                                                                 \
+    static bool attr2[3][2] = {{false, false}, {false, false}, {false, false}};
+#define FRSVT_LAUNCH_CMP2(EPIV, FSV)                                                                            \
   do {                                                                                                          \
-    if (!attr2[EPIV]) {                                                                                         \
-      CK(cudaFuncSetAttribute(tc::tc_compose2_kernel<EPIV>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+    if (!attr2[EPIV][FSV]) {                                                                                    \
+      CK(cudaFuncSetAttribute(tc::tc_compose2_kernel<EPIV, FSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                               (int)smem2));                                                                     \
-      attr2[EPIV] = true;                                                                                       \
+      attr2[EPIV][FSV] = true;                                                                                  \
     }                                                                                                           \
-    tc::tc_compose2_kernel<EPIV><<<grid, tc::CMP_THREADS, smem2, h->st>>>(                                      \
-        mQh, mQl, mWh, mWl, mD, mA, mE, (int)h->m, (int)h->n, &h->dev->r, nfull, sp, X, ldx, A, E, ld,        \
-        h->dev->mu, rho, lambda, h->redpart);                                                                   \
+    tc::tc_compose2_kernel<EPIV, FSV><<<grid, tc::CMP_THREADS, smem2, h->st>>>(                                 \
+        mQh, mQl, mWh, mWl, mD, mA, mE, mOm, (int)h->m, (int)h->n, h->l, &h->dev->r, nfull, sp, X, ldx, A, E, \
+        ld, h->dev->mu, rho, lambda, h->redpart, h->fspart, &h->dev->fs_done);                                  \
   } while (0)
-    if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP2(tc::EPI_ALM);
-    else FRSVT_LAUNCH_CMP2(tc::EPI_FINAL);
+    if (epi == tc::EPI_ALM && fs) FRSVT_LAUNCH_CMP2(tc::EPI_ALM, true);
+    else if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP2(tc::EPI_ALM, false);
+    else FRSVT_LAUNCH_CMP2(tc::EPI_FINAL, false);
 #undef FRSVT_LAUNCH_CMP2
     if (nparts) *nparts = (int)grid.x;
-    return post_launch(h);
+    TRY(post_launch(h));
+    if (fs) {
+      tc::fs_finish_kernel<<<(unsigned)rbs, 128, 0, h->st>>>(h->fspart, (int)h->m, h->l, &h->dev->r, nfull, sp,
+                                                              (float*)h->Y, &h->dev->fs_done);
+      TRY(post_launch(h));
+      h->fs_armed = true;
+    }
+    return FRSVT_OK;
   }
   const size_t smem = tc::ComposeSmem::total();
   static bool attr[3] = {false, false, false};
@@ -797,12 +819,16 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   h->override_pending = 0;
   if constexpr (sizeof(T) == 4) {
     if (rp_front) {
-      TRY(prof_begin(h));
+      // skipped on the device when the previous composition formed Y_p
+      // (dev->fs_done); such a launch is not counted in the pass profile
+      const int* skip = (h->fs_armed && ov == nullptr) ? &h->dev->fs_done : nullptr;
+      if (!skip) TRY(prof_begin(h));
       TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y, h->m,
-                                (const float*)h->Qt, h->m, 0, &h->dev->r));
-      TRY(prof_end(h, 0, (double)h->m * h->n * sizeof(T)));
+                                (const float*)h->Qt, h->m, 0, &h->dev->r, skip));
+      if (!skip) TRY(prof_end(h, 0, (double)h->m * h->n * sizeof(T)));
     }
   }
+  h->fs_armed = false;
   if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
   const bool sh = h->cfg.nranks > 1;
   h->t2_pending = 0;
@@ -1010,6 +1036,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
     CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
     CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
     h->call = 0;
+    h->fs_armed = false;
   }
   tau_from_mu_kernel<<<1, 1, 0, h->st>>>(h->dev->mu, &h->dev->tau);
   TRY(post_launch(h));
@@ -1020,8 +1047,20 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   bool done = false;
   if constexpr (sizeof(T) == 4) {
     if (h->use_tc) {
+      // fused next sketch: the next call's Omega and the carried columns of Y
+      // are set up here; the composition forms Y_p when p = l - r <= FS_PMAX
+      // (device-side decision) and the next sketch pass is then skipped
+      const bool fs_next = !finalize && h->fs && h->cmp2 && h->pass2 && h->rp != 0 && h->cfg.nranks == 1 &&
+                           tc_eligible(h, A, st->ld) && !h->override_pending;
+      if (fs_next) {
+        omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 1,
+                                                                    h->cfg.seed, 1000u + (uint32_t)h->call, nullptr,
+                                                                    h->n, 1);
+        TRY(post_launch(h));
+        CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
+      }
       TRY(tc_compose(h, finalize ? tc::EPI_FINAL : tc::EPI_ALM, (float*)st->L, st->ld, (const float*)D, (float*)A,
-                     (float*)E, st->ld, st->rho, lambda, &nparts));
+                     (float*)E, st->ld, st->rho, lambda, &nparts, fs_next));
       done = true;
     }
   }
@@ -1099,7 +1138,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->tilecnt, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->tilecnt, h->fspart, h->OmT, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1209,6 +1248,16 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->pass2 = !(e && e[0] == '0');
     const char* e8 = getenv("FRSVT_CMP2");
     h->cmp2 = !(e8 && e8[0] == '0');
+    const char* e9 = getenv("FRSVT_FS");
+    h->fs = !(e9 && e9[0] == '0');
+    h->fs_armed = false;
+    h->fspart_ctas = (size_t)cdiv(maxrows, 128) + 2 * (size_t)h->nsm + 8;
+    if (cudaMalloc((void**)&h->fspart, sizeof(float) * tc::FS_PMAX * 128 * h->fspart_ctas) != cudaSuccess ||
+        cudaMalloc((void**)&h->OmT, sizeof(float) * tc::FS_PMAX * (size_t)h->n) != cudaSuccess) {
+      cudaGetLastError();
+      free_handle(h);
+      return FRSVT_ENOMEM;
+    }
     const char* e7 = getenv("FRSVT_INFIX");
     h->infix = !(e7 && e7[0] == '0');
     h->ncnt = (int)cdiv(maxrows, 128) + 8;
@@ -1285,6 +1334,7 @@ void frsvt_destroy(frsvt_handle* h) {
 
 frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau, void* X, int64_t ldx,
                          frsvt_info* info) {
+  if (h) h->fs_armed = false;  // a fused next sketch belongs to rpca_alm_step
   if (!h || !A || !X || lda < h->m || ldx < h->m || !(tau >= 0) || !std::isfinite(tau)) return FRSVT_EINVAL;
   if (h->cfg.dtype == FRSVT_F32) return apply_impl<float>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
   return apply_impl<double>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
@@ -1293,6 +1343,7 @@ frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau
 frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda, int32_t wmode,
                                   const double* w, double C, double eps, void* X, int64_t ldx,
                                   frsvt_info* info) {
+  if (h) h->fs_armed = false;
   if (!h || !A || !X || lda < h->m || ldx < h->m) return FRSVT_EINVAL;
   int km;
   if (wmode == 0) {
@@ -1323,6 +1374,7 @@ frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, do
 
 frsvt_status frsvt_set_omega(frsvt_handle* h, const void* Om, int64_t ldo) {
   if (!h || !Om || ldo < h->n) return FRSVT_EINVAL;
+  h->fs_armed = false;  // a fused next sketch no longer matches
   CK(cudaMemcpy2DAsync(h->OmOv, h->n * h->esz, Om, ldo * h->esz, h->n * h->esz, h->l,
                        cudaMemcpyDeviceToDevice, h->st));
   h->override_pending = 1;
@@ -1331,6 +1383,7 @@ frsvt_status frsvt_set_omega(frsvt_handle* h, const void* Om, int64_t ldo) {
 
 frsvt_status frsvt_draw_omega(frsvt_handle* h, int64_t call, void* out, int64_t ldo) {
   if (!h || !out || ldo < h->n || call < 0) return FRSVT_EINVAL;
+  h->fs_armed = false;  // h->Om is overwritten
   if (h->cfg.dtype == FRSVT_F32)
     omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 0,
                                                                h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n);
@@ -1359,6 +1412,7 @@ frsvt_status frsvt_get_carry(frsvt_handle* h, void* Qt, int64_t ldq, int32_t* r)
 
 frsvt_status frsvt_set_carry(frsvt_handle* h, const void* Qt, int64_t ldq, int32_t r) {
   if (!h || r < 0 || r > h->l || (r > 0 && (!Qt || ldq < h->m))) return FRSVT_EINVAL;
+  h->fs_armed = false;  // a fused next sketch no longer matches
   CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
   if (r > 0)
     CK(cudaMemcpy2DAsync(h->Qt, h->m * h->esz, Qt, ldq * h->esz, h->m * h->esz, r, cudaMemcpyDeviceToDevice,
@@ -1370,6 +1424,7 @@ frsvt_status frsvt_set_carry(frsvt_handle* h, const void* Qt, int64_t ldq, int32
 
 frsvt_status frsvt_reset_carry(frsvt_handle* h) {
   if (!h) return FRSVT_EINVAL;
+  h->fs_armed = false;  // a fused next sketch no longer matches
   CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
   CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
   CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
@@ -1378,6 +1433,7 @@ frsvt_status frsvt_reset_carry(frsvt_handle* h) {
 
 frsvt_status frsvt_set_call_index(frsvt_handle* h, int64_t call) {
   if (!h || call < 0) return FRSVT_EINVAL;
+  h->fs_armed = false;  // a fused next sketch no longer matches
   h->call = call;
   return FRSVT_OK;
 }
@@ -1396,6 +1452,7 @@ frsvt_status rpca_get_mu(frsvt_handle* h, double* mu) {
 
 frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar) {
   if (!h || !(mu > 0) || !(mu_bar >= mu)) return FRSVT_EINVAL;
+  h->fs_armed = false;
   double v[2] = {mu, mu_bar};
   CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(h->dev->mu, v, sizeof(v), cudaMemcpyHostToDevice));

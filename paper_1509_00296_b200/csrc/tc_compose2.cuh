@@ -35,25 +35,52 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "memory");
 }
 
+// d = a * b + c on fp32 pairs (FFMA2)
+__device__ __forceinline__ uint64_t ffma2_u64(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// Omega^T (rows 0..n-1, FS_PMAX columns each, zero past l) for the fused sketch's TMA slices
+__global__ void omega_t24_kernel(const float* __restrict__ Om, int64_t n, int l, float* __restrict__ OmT) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * 24) return;
+  const int64_t c = idx / 24;
+  const int j = (int)(idx - c * 24);
+  OmT[idx] = j < l ? Om[c + (int64_t)j * n] : 0.f;
+}
+
 constexpr int C2_RING = 12;                     // D/A/E slice stages
 constexpr uint32_t C2_SLICE = 128u * 8u * 4u;  // one array, 128 rows x 8 columns = 4 KB
+constexpr int FS_PMAX = 24;                     // fused next sketch: at most this many fresh columns
+constexpr uint32_t C2_OM = 8u * FS_PMAX * 4u;   // Omega rows of a slice: 8 x 24 fp32 = 768 B
+constexpr uint32_t C2_STAGE = 3 * C2_SLICE + C2_OM;
 
 struct Compose2Smem {
   static constexpr uint32_t chunk_bytes = 128u * BK * 4u;  // 16 KB (Wt / Q~ chunk)
-  __host__ __device__ static constexpr size_t ring_bytes() { return (size_t)C2_RING * 3 * C2_SLICE; }  // 144 KB >= Q~ staging (128 KB)
+  __host__ __device__ static constexpr size_t ring_bytes() { return (size_t)C2_RING * C2_STAGE; }  // 153 KB >= Q~ staging (128 KB)
   __host__ __device__ static constexpr size_t total() {
     return 1024 + ring_bytes() + (size_t)CMP_WSTAGES * 2 * chunk_bytes + 1024;
   }
 };
 
-template <int EPI>
+// FS (EPI_ALM only): also form the next call's fresh sketch Y_p = A' Omega_p
+// (Alg. 1 line 4 / the RP branch P:132-135 for the next iALM iteration;
+// SURVEY §8(a)-a9 "optional partial A' Omega'_p") from the A' values this
+// epilogue computes anyway, when p = l - r <= FS_PMAX: fp32 FMAs over the
+// CTA's columns, one partial row block per CTA in fspart (summed in CTA order
+// by fs_finish_kernel); *fs_done says whether it was formed.
+template <int EPI, bool FS>
 __global__ void __launch_bounds__(CMP_THREADS, 1)
 tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_constant__ CUtensorMap mapQl,
                    const __grid_constant__ CUtensorMap mapWh, const __grid_constant__ CUtensorMap mapWl,
                    const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapE, int m, int n, const int* __restrict__ r_dev, int nfull,
-                   int sp, float* __restrict__ X, int64_t ldx, float* __restrict__ Aop, float* __restrict__ E,
-                   int64_t ld, const double* __restrict__ mu, double rho, double lambda, double* __restrict__ part) {
+                   const __grid_constant__ CUtensorMap mapE, const __grid_constant__ CUtensorMap mapOm, int m, int n,
+                   int l, const int* __restrict__ r_dev, int nfull, int sp, float* __restrict__ X, int64_t ldx,
+                   float* __restrict__ Aop, float* __restrict__ E, int64_t ld, const double* __restrict__ mu,
+                   double rho, double lambda, double* __restrict__ part, float* __restrict__ fspart,
+                   int* __restrict__ fs_done) {
   static_assert(EPI == EPI_ALM || EPI == EPI_FINAL, "compose2 streams D/E(/A)");
   constexpr uint32_t CB = Compose2Smem::chunk_bytes;
   constexpr int NARR = EPI == EPI_ALM ? 3 : 2;  // D, E (, A)
@@ -90,6 +117,8 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
   const int r = *r_dev;
   const int nk = (r + BK - 1) / BK;  // K chunks actually used (r <= Kp <= 128)
   const int nsl = (jt1 - jt0) * 16;  // 8-column slices of this CTA
+  const int pfs = l - r;             // fresh columns of the next sketch
+  const bool fs = FS && EPI == EPI_ALM && pfs >= 1 && pfs <= FS_PMAX;
 
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
@@ -149,6 +178,7 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
       prefetch_tmap(&mapD);
       prefetch_tmap(&mapE);
       if (EPI == EPI_ALM) prefetch_tmap(&mapA);
+      if (fs) prefetch_tmap(&mapOm);
       const uint64_t pol = l2_policy_evict_first();
       if (nk > 0) mbar_wait(qready, 0);  // Q~ staging in the ring has been consumed
       for (int i = 0; i < nsl; ++i) {
@@ -156,11 +186,12 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
         const uint32_t ph = (i / C2_RING) & 1;
         mbar_wait(&sempty[s], ph ^ 1);
         const int c0 = jt0 * 128 + 8 * i;
-        uint8_t* st = ring + (size_t)s * 3 * C2_SLICE;
-        mbar_expect_tx(&sfull[s], NARR * C2_SLICE);
+        uint8_t* st = ring + (size_t)s * C2_STAGE;
+        mbar_expect_tx(&sfull[s], NARR * C2_SLICE + (fs ? C2_OM : 0u));
         tma_load_2d_hint(st, &mapD, &sfull[s], rb * 128, c0, pol);
         tma_load_2d_hint(st + C2_SLICE, &mapE, &sfull[s], rb * 128, c0, pol);
         if (EPI == EPI_ALM) tma_load_2d_hint(st + 2 * C2_SLICE, &mapA, &sfull[s], rb * 128, c0, pol);
+        if (fs) tma_load_2d(st + 3 * C2_SLICE, &mapOm, &sfull[s], 0, c0);  // Omega^T: rows c0..c0+7, 24 columns each
       }
     }
   } else if (warp == 1) {
@@ -234,6 +265,9 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
     }
     const float fratio = (float)ratio, fthr = (float)thr;
     double resid = 0.0;
+    uint64_t ys[FS ? FS_PMAX / 2 : 1];  // fp32 pairs (j = 2q, 2q + 1)
+#pragma unroll
+    for (int q = 0; q < (FS ? FS_PMAX / 2 : 1); ++q) ys[q] = 0ull;
     for (int i = grp; i < nsl; i += 4) {
       const int tl = i >> 4, cc = i & 15, b = tl & 1;
       const int s = i % C2_RING;
@@ -255,7 +289,7 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
         for (int jj = 0; jj < 8; ++jj) v[jj] = 0u;
       }
       mbar_wait(&sfull[s], (i / C2_RING) & 1);
-      const float* st = reinterpret_cast<const float*>(ring + (size_t)s * 3 * C2_SLICE);
+      const float* st = reinterpret_cast<const float*>(ring + (size_t)s * C2_STAGE);
       float dv[8], ev[8], av[8];
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
@@ -263,8 +297,11 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
         ev[jj] = st[1024 + jj * 128 + rloc];
         av[jj] = EPI == EPI_ALM ? st[2048 + jj * 128 + rloc] : 0.f;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sempty[s]);
+      if (!fs) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s]);
+      }
+      float an[8];  // A' of this slice (fused sketch)
       if (row < m) {
         const int c0 = (jt0 + tl) * 128 + 8 * cc;
 #pragma unroll
@@ -280,11 +317,58 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
             } else {
               const float rr = (av[jj] - Lv) * fratio;
               const float en = soft<float>(dv[jj] - Lv + rr, fthr);
+              an[jj] = dv[jj] - en + rr;
               __stcs(E + o, en);
-              __stcs(Aop + o, dv[jj] - en + rr);
+              __stcs(Aop + o, an[jj]);
+            }
+          } else {
+            an[jj] = 0.f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) an[jj] = 0.f;
+      }
+      if (FS && fs) {
+        // ys[j] += sum_jj A'(row, c0 + jj) Omega(c0 + jj, j): packed fp32 pairs
+        // (FFMA2), Omega^T rows of the slice in shared memory ([jj][24], zero
+        // past n)
+        const float* om = st + 3 * 1024;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const float2 a2 = make_float2(an[jj], an[jj]);
+          const uint64_t a = *reinterpret_cast<const uint64_t*>(&a2);
+#pragma unroll
+          for (int t = 0; t < FS_PMAX / 4; ++t) {
+            if (4 * t < pfs) {
+              const float4 o = *reinterpret_cast<const float4*>(om + jj * FS_PMAX + 4 * t);
+              const float2 o01 = make_float2(o.x, o.y), o23 = make_float2(o.z, o.w);
+              ys[2 * t] = ffma2_u64(a, *reinterpret_cast<const uint64_t*>(&o01), ys[2 * t]);
+              ys[2 * t + 1] = ffma2_u64(a, *reinterpret_cast<const uint64_t*>(&o23), ys[2 * t + 1]);
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s]);
+      }
+    }
+    if (FS && fs) {
+      // the four groups' partial rows -> this CTA's slot: ring reused as scratch
+      // once every epilogue warp is past its last slice
+      asm volatile("bar.sync 1, 512;" ::: "memory");
+      float* scr = reinterpret_cast<float*>(ring);  // [grp][j][128]
+#pragma unroll
+      for (int q = 0; q < FS_PMAX / 2; ++q) {
+        const float2 y = *reinterpret_cast<const float2*>(&ys[q]);
+        if (2 * q < pfs) scr[(grp * FS_PMAX + 2 * q) * 128 + rloc] = y.x;
+        if (2 * q + 1 < pfs) scr[(grp * FS_PMAX + 2 * q + 1) * 128 + rloc] = y.y;
+      }
+      asm volatile("bar.sync 1, 512;" ::: "memory");
+      if (grp == 0) {
+        float* dst = fspart + (size_t)blockIdx.x * FS_PMAX * 128;
+        for (int j = 0; j < pfs; ++j)
+          dst[j * 128 + rloc] = ((scr[(0 * FS_PMAX + j) * 128 + rloc] + scr[(1 * FS_PMAX + j) * 128 + rloc]) +
+                                 scr[(2 * FS_PMAX + j) * 128 + rloc]) + scr[(3 * FS_PMAX + j) * 128 + rloc];
       }
     }
     resid = warp_sum(resid);
@@ -296,10 +380,28 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
     double s = 0.0;
     for (int w = 4; w < CMP_THREADS / 32; ++w) s += red[w];
     part[blockIdx.x] = s;
+    if (FS && blockIdx.x == 0) *fs_done = fs ? 1 : 0;
   }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tbase, 512);
+  }
+}
+
+// Y[:, r + j] (j < p) = sum of the covering CTAs' partial rows, in CTA order
+// (the compose2 grid: CTA rb for rb < nfull, else nfull + (rb - nfull) sp + e).
+__global__ void __launch_bounds__(128) fs_finish_kernel(const float* __restrict__ fspart, int m, int l,
+                                                        const int* __restrict__ r_dev, int nfull, int sp,
+                                                        float* __restrict__ Y, const int* __restrict__ fs_done) {
+  if (!*fs_done) return;
+  const int r = *r_dev, p = l - r;
+  const int rb = blockIdx.x, rloc = threadIdx.x, row = rb * 128 + rloc;
+  const int c0 = rb < nfull ? rb : nfull + (rb - nfull) * sp;
+  const int nc = rb < nfull ? 1 : sp;
+  for (int j = 0; j < p; ++j) {
+    float y = 0.f;
+    for (int e = 0; e < nc; ++e) y += fspart[((size_t)(c0 + e) * FS_PMAX + j) * 128 + rloc];
+    if (row < m) Y[row + (int64_t)(r + j) * m] = y;
   }
 }
 

@@ -51,11 +51,17 @@
 namespace frsvt {
 namespace tc {
 
-constexpr int P2_ASTAGES = 4;  // A ring (16 KB stages; released by the converters)
+#ifndef P2_AST
+#define P2_AST 4
+#endif
+#ifndef P2_BST
+#define P2_BST 5
+#endif
+constexpr int P2_ASTAGES = P2_AST;  // A ring (16 KB stages; released by the converters; even)
 // B ring: released by the MMA. Its depth must cover MMA completion (~700
 // cycles) + the L2 latency of the small operand under the A stream (~1900
 // cycles, clock64 stamps): 5 stages of (roundup8(l) rows x 256 B)
-constexpr int P2_BSTAGES = 5;
+constexpr int P2_BSTAGES = P2_BST;
 constexpr int P2_TSTAGES = 4;  // TMEM A ring (64 columns per stage: a_h tf32 | bf16 a_h | bf16 a_l)
 constexpr int P2_SEG = 8;      // chunks accumulated in TMEM before a flush
 constexpr int P2_THREADS = 640;
@@ -197,7 +203,9 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
                 const __grid_constant__ CUtensorMap mapBl, int Mtot, int Ktot, int Nvalid, int nbrows,
                 float* __restrict__ out, int64_t ldo, const float* __restrict__ add, int64_t ldadd,
                 float* __restrict__ part, const int* __restrict__ rp_dev, int dbg,
-                unsigned int* __restrict__ tile_cnt) {
+                unsigned int* __restrict__ tile_cnt, const int* __restrict__ skip_dev) {
+  // skip_dev (nullable): the output was already formed (fused next sketch)
+  if (skip_dev && *skip_dev) return;
   // tile_cnt (nullable, >= mtiles zeros): in-kernel stream-K fixup. The CTA
   // that completes the last partial segment of a split tile sums all its
   // partial slots in CTA order (deterministic), writes the tile and re-arms
