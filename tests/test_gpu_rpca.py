@@ -113,3 +113,22 @@ def test_rpca_c2_trajectory(P):
     assert resid[-1] <= 1e-6
     L0 = d["L0"].numpy()
     assert np.linalg.norm(np64(L) - L0) / np.linalg.norm(L0) <= 1e-4
+
+
+def test_fused_next_sketch_matches_pass(P, monkeypatch):
+    """The fused next sketch (Y_p = A' Omega_p formed in the iALM epilogue when
+    p = l - r <= 24) against the same solve with it disabled
+    (FRSVT_FS=0, the sketch by the tensor-core pass): identical kept ranks,
+    L, E and residuals within fp32 rounding of the two summation orders."""
+    cfg, d = make_config("c5", m=6144, n=768, rank=24, l=40, iters=30, var=1.0 / 6144)
+    D = cm(d["D"], torch.float32)
+    n2 = oracle.norm2_power(np64(D))
+    out = {}
+    for fs in ("1", "0"):
+        monkeypatch.setenv("FRSVT_FS", fs)
+        h, L, E, resid = _run_gpu(P, cfg, D, n2, cfg.iters, rho=cfg.params["rho"])
+        out[fs] = (h.info().r, np64(L), np64(E), np.array(resid))
+    assert out["1"][0] == out["0"][0] and out["1"][0] >= 24 and cfg.l - out["1"][0] <= 24  # fused in steady state
+    for i in (1, 2):
+        assert np.linalg.norm(out["1"][i] - out["0"][i]) <= 1e-4 * np.linalg.norm(out["0"][i])
+    assert np.allclose(out["1"][3], out["0"][3], rtol=1e-2, atol=1e-8)
