@@ -134,8 +134,8 @@ frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda,
  * mu_0 (mu0, else 1.25/||D||_2), E_1, A_1. finalize != 0 writes L_{k+1} into
  * st->L and leaves D, E, A, mu untouched (the textbook state after k+1 steps).
  * D, E, A, L: m_local x n, leading dim ld. rel_resid: host, nullable (syncs).
- * Fused next sketch (fp32 tensor path, range propagation, one rank; on unless
- * FRSVT_FS=0): when p = l - r <= 24 the epilogue also forms the next call's
+ * Fused next sketch (opt-in, FRSVT_FS=1; fp32 tensor path, range propagation,
+ * one rank): when p = l - r <= 24 the epilogue also forms the next call's
  * fresh sketch A_{k+1} Omega_p and the next step skips that
  * pass. The contents of A (library-managed) must therefore not be changed by
  * the caller between consecutive steps unless a state setter runs in between

@@ -117,8 +117,8 @@ def test_rpca_c2_trajectory(P):
 
 def test_fused_next_sketch_matches_pass(P, monkeypatch):
     """The fused next sketch (Y_p = A' Omega_p formed in the iALM epilogue when
-    p = l - r <= 24) against the same solve with it disabled
-    (FRSVT_FS=0, the sketch by the tensor-core pass): identical kept ranks,
+    p = l - r <= 24; opt-in FRSVT_FS=1) against the same
+    solve with it disabled (FRSVT_FS=0, the sketch by the tensor-core pass): identical kept ranks,
     L, E and residuals within fp32 rounding of the two summation orders."""
     cfg, d = make_config("c5", m=6144, n=768, rank=24, l=40, iters=30, var=1.0 / 6144)
     D = cm(d["D"], torch.float32)
