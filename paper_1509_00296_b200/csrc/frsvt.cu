@@ -566,9 +566,10 @@ template <typename T>
 frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded, const int* r_dev = nullptr) {
   const int l = h->l;
   if (h->dmma_gram) {  // fp64 tensor cores, upper 8x8 blocks only (gram_dmma.cuh)
-    int S = (int)cdiv(rows, 256);
+    // one wave (1 CTA of 256 threads per SM at ~250 registers), >= 32 rows each
+    int S = (int)cdiv(rows, GD_ROWS);
     const int Smax = (int)(h->partd_elems / ((size_t)l * l));
-    if (S > 2 * h->nsm) S = 2 * h->nsm;
+    if (S > h->nsm) S = h->nsm;
     if (S > Smax) S = Smax;
     if (S < 1) S = 1;
     const int64_t rpc = cdiv(cdiv(rows, S), GD_ROWS) * GD_ROWS;
