@@ -43,6 +43,18 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _traffic(kernel):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json: dram__bytes_read.sum +
+    dram__bytes_write.sum), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    e = d.get(kernel)
+    return float(e["bytes_per_launch"]) if e else None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -303,7 +315,7 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": _config_dict(cfg, ws),
                 "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                             "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                             "unit": "GB/s", "frac": achieved / peak, "traffic": _traffic(dom),
                              "peak_source": peak_src, "per_pass": per_pass},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}

@@ -84,7 +84,9 @@ __device__ __forceinline__ int eig_col_at(bool top, int q, int k, int L2) {
 __global__ void __launch_bounds__(512, 1)
 eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict__ t_dev, double t_host,
                   int t_mode, double tol_rot, double tol_stop, int max_sweeps, double* __restrict__ sigma,
-                  double* __restrict__ UB, int* __restrict__ sweeps_out, int* __restrict__ flags) {
+                  double* __restrict__ UB, int* __restrict__ sweeps_out, int* __restrict__ flags,
+                  const int* __restrict__ run_if = nullptr) {
+  if (run_if && !*run_if) return;  // (warm-start block solve, eig_warm.cuh) not needed
   constexpr int PPW = EIG_PPW;
   extern __shared__ double esm[];
   const int nw = blockDim.x >> 5;

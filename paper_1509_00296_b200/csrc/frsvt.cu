@@ -16,6 +16,7 @@
 #include "small.cuh"
 #include "small2.cuh"
 #include "eig_jacobi.cuh"
+#include "eig_warm.cuh"
 #include "orth_chol.cuh"
 #include "lowdin.cuh"
 #include "chol_fast.cuh"
@@ -78,6 +79,8 @@ struct frsvt_handle {
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
   int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
   int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
+  int warm_eig;      // 1: warm-started small SVD under range propagation (eig_warm.cuh, FRSVT_WARM_EIG)
+  double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_FS=1)
   bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
   float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
@@ -903,6 +906,25 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     TRY(gemm_ll<double>(h, h->G, 0, h->T2d, 0, h->Hd));
     TRY(gemm_ll<double>(h, h->T2d, 1, h->Hd, 0, h->G));
   }
+  if (h->warm_eig && h->rp != 0) {
+    // warm start (R16): diagonalise the fresh block first, solve the rotated Gram
+    int* flag = h->lwd + 6;
+    eig_fresh_pack_kernel<<<1, 256, 0, h->st>>>(h->G, h->l, &h->dev->r, h->ewbuf, flag);
+    TRY(post_launch(h));
+    double* Gpad = h->ewbuf;
+    double* Uf = Gpad + EW_P * EW_P;
+    double* sigf = Uf + EW_P * EW_P;
+    double* G2 = sigf + EW_P;
+    eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(EW_P), EigJacobi::smem_bytes(EW_P), h->st>>>(
+        Gpad, EW_P, nullptr, 0.0, 0, 1e-15, 0.0, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag);
+    TRY(post_launch(h));
+    eig_fresh_rotate_kernel<<<(unsigned)cdiv((int64_t)h->l * h->l, 256), 256, 0, h->st>>>(h->G, h->l, &h->dev->r,
+                                                                                          Uf, flag, G2);
+    TRY(post_launch(h));
+    TRY(launch_eig(h, 0, G2, h->sigma, h->UB, t_mode, t_host, t_dev));
+    eig_fresh_back_kernel<<<(unsigned)cdiv(h->l, 128), 128, 0, h->st>>>(h->UB, h->l, &h->dev->r, Uf, flag);
+    return post_launch(h);
+  }
   return launch_eig(h, 0, h->G, h->sigma, h->UB, t_mode, t_host, t_dev);
 }
 
@@ -1139,7 +1161,7 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
 static void free_handle(frsvt_handle* h) {
   if (!h) return;
   void* ptrs[] = {h->Om, h->OmOv, h->Y, h->Q, h->Qtmp, h->Qt, h->Z, h->Zq, h->Zt, h->Wt, h->T1, h->Mc,
-                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->tilecnt, h->fspart, h->OmT, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
+                  h->Mp, h->wvec, h->Xh, h->Xl, h->Qh, h->Ql, h->QtTh, h->QtTl, h->WtTh, h->WtTl, h->partq, h->partd, h->redpart, h->skpart, h->Xb, h->Qb, h->tilecnt, h->fspart, h->OmT, h->ewbuf, h->E2b, h->Rf, h->T2d, h->Hd, h->McD, h->MpD, h->lwd, h->G, h->UB, h->sigma, h->dprev,
                   h->redtmp, h->dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1247,6 +1269,13 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->nsm = nsm;
     const char* e = getenv("FRSVT_PASS2");
     h->pass2 = !(e && e[0] == '0');
+    const char* e11 = getenv("FRSVT_WARM_EIG");
+    h->warm_eig = !(e11 && e11[0] == '0');
+    if (cudaMalloc((void**)&h->ewbuf, sizeof(double) * (2 * EW_P * EW_P + EW_P + (size_t)l * l)) != cudaSuccess) {
+      cudaGetLastError();
+      free_handle(h);
+      return FRSVT_ENOMEM;
+    }
     const char* e8 = getenv("FRSVT_CMP2");
     h->cmp2 = !(e8 && e8[0] == '0');
     const char* e9 = getenv("FRSVT_FS");  // opt-in: +0.5-1% iter/s on c5, at the cost of a slower composition
