@@ -132,3 +132,23 @@ def test_fused_next_sketch_matches_pass(P, monkeypatch):
     for i in (1, 2):
         assert np.linalg.norm(out["1"][i] - out["0"][i]) <= 1e-4 * np.linalg.norm(out["0"][i])
     assert np.allclose(out["1"][3], out["0"][3], rtol=1e-2, atol=1e-8)
+
+
+def test_warm_small_svd_matches_cold(P, monkeypatch):
+    """The warm-started small SVD under range propagation (fresh Gram block
+    diagonalised first, R16) against the plain Jacobi on the Gram
+    (FRSVT_WARM_EIG=0): same kept ranks, L and E within the parity bar, and
+    fewer sweeps in the steady state."""
+    cfg, d = make_config("c5", m=6144, n=768, rank=24, l=40, iters=30, var=1.0 / 6144)
+    D = cm(d["D"], torch.float32)
+    n2 = oracle.norm2_power(np64(D))
+    out = {}
+    for warm in ("1", "0"):
+        monkeypatch.setenv("FRSVT_WARM_EIG", warm)
+        h, L, E, resid = _run_gpu(P, cfg, D, n2, cfg.iters - 1, rho=cfg.params["rho"])
+        sweeps = h.info().sweeps          # the last (non-finalize) step's solve
+        out[warm] = (h.info().r, np64(L), np64(E), sweeps)
+    assert out["1"][0] == out["0"][0] and 2 <= cfg.l - out["1"][0] <= 32  # the warm path applies
+    for i in (1, 2):
+        assert np.linalg.norm(out["1"][i] - out["0"][i]) <= 1e-4 * np.linalg.norm(out["0"][i])
+    assert out["1"][3] < out["0"][3]
