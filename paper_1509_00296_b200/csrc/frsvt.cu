@@ -81,6 +81,7 @@ struct frsvt_handle {
   int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
   int warm_eig;      // 1: warm-started small SVD under range propagation (eig_warm.cuh, FRSVT_WARM_EIG)
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
+  double ew_rot, ew_stop;  // fresh-block solve tolerances (the full solve refines)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_FS=1)
   bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
   float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
@@ -916,7 +917,7 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     double* sigf = Uf + EW_P * EW_P;
     double* G2 = sigf + EW_P;
     eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(EW_P), EigJacobi::smem_bytes(EW_P), h->st>>>(
-        Gpad, EW_P, nullptr, 0.0, 0, 1e-15, 0.0, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag);
+        Gpad, EW_P, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag);
     TRY(post_launch(h));
     eig_fresh_rotate_kernel<<<(unsigned)cdiv((int64_t)h->l * h->l, 256), 256, 0, h->st>>>(h->G, h->l, &h->dev->r,
                                                                                           Uf, flag, G2);
@@ -1271,6 +1272,12 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     h->pass2 = !(e && e[0] == '0');
     const char* e11 = getenv("FRSVT_WARM_EIG");
     h->warm_eig = !(e11 && e11[0] == '0');
+    // fresh-block solve: fp32 handles as the main solve (R3; the full solve
+    // refines), fp64 handles to 1e-15; FRSVT_EW_TOL="rot,stop" overrides
+    const char* e12 = getenv("FRSVT_EW_TOL");
+    h->ew_rot = c.dtype == FRSVT_F32 ? 1e-9 : 1e-15;
+    h->ew_stop = c.dtype == FRSVT_F32 ? 1e-4 : 0.0;
+    if (e12) sscanf(e12, "%lf,%lf", &h->ew_rot, &h->ew_stop);
     if (cudaMalloc((void**)&h->ewbuf, sizeof(double) * (2 * EW_P * EW_P + EW_P + (size_t)l * l)) != cudaSuccess) {
       cudaGetLastError();
       free_handle(h);
