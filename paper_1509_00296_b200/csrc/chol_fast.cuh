@@ -1,96 +1,14 @@
-// CholeskyQR first pass without an explicit inverse (fp32 handles):
-//   chol_rows_kernel : R' of the equilibrated Gram, one CTA, register resident
-//   trsm_rows_kernel : Q1 = Y R'^{-1}, one thread per row of Y, 32-column blocks
-//
-// The factor ("QR_CP", reading R4): unpivoted Cholesky
-// of S = diag(dsc) G diag(dsc), dsc_i = G_ii^{-1/2}, with column drop: a
-// column whose Schur diagonal is <= tol (relative to its own norm^2) gets a
-// zero row in R (a zero column in Q1). Only the span of Q1 matters downstream
-// (Prop. 1). R' = R diag(dsc)^{-1}, so Y R'^{-1} = Y diag(dsc) R^{-1}.
-//
-// chol_rows_kernel: each of the 1024 threads owns <= 9 entries (i <= j) of the
-// upper triangle of S in registers. Step k reads row k of the current Schur
-// complement from a double-buffered shared row, every thread forms
-// 1/S_kk itself, updates its entries with i > k by S_ij -= S_ki S_kj / S_kk,
-// and the owners of row k+1 publish it: one block barrier per step. The owner
-// of (k, j) writes R'_kj = S_kj / sqrt(S_kk) / dsc_j at step k.
+// CholeskyQR first pass without an explicit inverse (fp32 handles,
+// FRSVT_FASTCHOL=1; the default is chol_inv.cuh + a tensor-core apply):
+//   trsm_rows_kernel : Q1 = Y R'^{-1}, one thread per row of Y, 32-column blocks,
+// with R' from orth_chol_kernel's R mode ("QR_CP",
+// reading R4): R' = R diag(dsc)^{-1} of the equilibrated Gram's Cholesky factor
+// with column drop, so Y R'^{-1} = Y diag(dsc) R^{-1}. Only the span of Q1
+// matters downstream (Prop. 1).
 #pragma once
 #include "common.cuh"
 
 namespace frsvt {
-
-constexpr int CHR_THREADS = 1024;
-constexpr int CHR_PER = (FRSVT_LMAX * (FRSVT_LMAX + 1) / 2 + CHR_THREADS - 1) / CHR_THREADS;  // 9
-
-__global__ void __launch_bounds__(CHR_THREADS, 1)
-chol_rows_kernel(const double* __restrict__ G, int l, double tol, double* __restrict__ Rp, int* __restrict__ s_out,
-                 int* __restrict__ flags, const int* __restrict__ skip) {
-  if (skip && *skip) return;
-  __shared__ double dsc[FRSVT_LMAX];
-  __shared__ double row[2][FRSVT_LMAX];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < l; i += CHR_THREADS) {
-    const double g = G[i + (size_t)i * l];
-    if (!isfinite(g)) atomicOr(flags, FLAG_NONFINITE);
-    dsc[i] = (g > 0.0 && isfinite(g)) ? rsqrt(g) : 0.0;
-  }
-  __syncthreads();
-  // owned entries: e = tid + CHR_THREADS q of the row-major upper triangle
-  double s[CHR_PER];
-  int ij[CHR_PER];  // (i << 16) | j, or -1
-  const int ntri = l * (l + 1) / 2;
-#pragma unroll
-  for (int q = 0; q < CHR_PER; ++q) {
-    const int e = tid + CHR_THREADS * q;
-    int i = -1, j = -1;
-    if (e < ntri) {
-      // row i starts at base(i) = i l - i (i - 1) / 2; invert the prefix sum
-      const double b2 = 2.0 * l + 1.0;
-      int ri = (int)floor(0.5 * (b2 - sqrt(b2 * b2 - 8.0 * e)));
-      ri = max(0, min(l - 1, ri));
-      while (ri > 0 && ri * l - ri * (ri - 1) / 2 > e) --ri;
-      while (ri + 1 < l && (ri + 1) * l - (ri + 1) * ri / 2 <= e) ++ri;
-      i = ri;
-      j = ri + (e - (ri * l - ri * (ri - 1) / 2));
-    }
-    ij[q] = i >= 0 ? ((i << 16) | j) : -1;
-    double v = 0.0;
-    if (i >= 0) {
-      v = G[i + (size_t)j * l] * dsc[i] * dsc[j];
-      if (!isfinite(v)) v = 0.0;
-      if (i == 0) row[0][j] = v;
-    }
-    s[q] = v;
-  }
-  __syncthreads();
-  int kept = 0;
-  for (int k = 0; k < l; ++k) {
-    const double* rk = row[k & 1];
-    double* rn = row[(k + 1) & 1];
-    const double d = rk[k];
-    const bool ok = d > tol;
-    const double dinv = ok ? 1.0 / d : 0.0;
-    const double rin = ok ? rsqrt(d) : 0.0;
-    if (tid == 0) kept += ok ? 1 : 0;
-#pragma unroll
-    for (int q = 0; q < CHR_PER; ++q) {
-      const int i = ij[q] >= 0 ? (ij[q] >> 16) : -1, j = ij[q] & 0xFFFF;
-      if (i == k) {  // row k of R' (final)
-        Rp[(size_t)k * l + j] = (ok && dsc[j] > 0.0) ? s[q] * rin / dsc[j] : 0.0;
-      } else if (i > k) {
-        s[q] = fma(-rk[i] * dinv, rk[j], s[q]);
-        if (i == k + 1) rn[j] = s[q];
-      }
-    }
-    __syncthreads();
-  }
-  // lower triangle of R' is zero
-  for (int idx = tid; idx < l * l; idx += CHR_THREADS) {
-    const int i = idx / l, j = idx % l;
-    if (j < i) Rp[idx] = 0.0;
-  }
-  if (tid == 0) *s_out = kept;
-}
 
 // Q (rows x l) = Y R'^{-1}: q R' = y by forward substitution, one thread per
 // row. The row is processed in NB blocks of 32 columns (fully unrolled); a
