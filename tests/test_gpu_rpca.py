@@ -152,3 +152,37 @@ def test_warm_small_svd_matches_cold(P, monkeypatch):
     for i in (1, 2):
         assert np.linalg.norm(out["1"][i] - out["0"][i]) <= 1e-4 * np.linalg.norm(out["0"][i])
     assert out["1"][3] < out["0"][3]
+
+
+def test_solve_replays_as_cuda_graph(P):
+    """A whole iALM solve (init, steps, finalize) captured into one CUDA graph
+    and replayed (how bench.py times it) gives the same L and E as the eager
+    launches: the library allocates nothing and never synchronises inside
+    rpca_alm_step, and its kernels are deterministic."""
+    cfg, d = make_config("c5", m=6144, n=768, rank=24, l=40, iters=12, var=1.0 / 6144)
+    D = cm(d["D"], torch.float32)
+    m, n = D.shape
+    n2 = oracle.norm2_power(np64(D))
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        h = P.Frsvt(m, n, cfg.l, cfg.q, rp=True, dtype=torch.float32, seed=cfg.seed, stream=stream)
+        E, A, L = torch.empty_like(D), torch.empty_like(D), torch.empty_like(D)
+
+    def solve():
+        st = h.rpca_state(D, E, A, L, rho=cfg.params["rho"], norm2_D=n2)
+        for k in range(cfg.iters):
+            h.rpca_step(st, finalize=(k == cfg.iters - 1))
+
+    with torch.cuda.stream(stream):
+        solve()
+    stream.synchronize()
+    L_eager, E_eager = L.clone(), E.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+        solve()
+    L.zero_()
+    E.zero_()
+    with torch.cuda.stream(stream):
+        g.replay()
+    stream.synchronize()
+    assert torch.equal(L, L_eager) and torch.equal(E, E_eager)
