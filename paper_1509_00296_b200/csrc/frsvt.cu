@@ -493,7 +493,9 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   if (sp > ntiles) sp = ntiles;
   if (sp < 1) sp = 1;
   dim3 grid((unsigned)(nfull + rem * sp));
-  if (h->cmp2 && epi != tc::EPI_STORE) {
+  // compose2 streams D, A, E through TMA: 16-byte aligned columns required
+  const bool tma_ok = (ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0;
+  if (h->cmp2 && epi != tc::EPI_STORE && tma_ok) {
     CUtensorMap mD, mA, mE;
     if (!make_map(&mD, D, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mE, E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||

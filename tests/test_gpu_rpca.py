@@ -186,3 +186,24 @@ def test_solve_replays_as_cuda_graph(P):
         g.replay()
     stream.synchronize()
     assert torch.equal(L, L_eager) and torch.equal(E, E_eager)
+
+
+@pytest.mark.parametrize("m,n", [(1000, 997), (999, 640), (1280, 1536)])
+def test_rpca_ragged_shapes(P, m, n):
+    """Free-running iALM against the oracle on shapes that exercise the edges of
+    the tensor path: n not a multiple of the composition's 8-column TMA slices
+    (1000 x 997), an operand whose column stride is not 16-byte aligned
+    (999 rows: the SIMT passes and the per-thread-load composition), and whole
+    tiles (1280 x 1536)."""
+    cfg, d = make_config("c2", m=m, n=n, rank=20, l=40, iters=16)
+    D = cm(d["D"], torch.float32)
+    D64 = np64(D)
+    L0 = d["L0"].numpy()
+    n2 = oracle.norm2_power(D64)
+    ref = oracle.rpca_ialm(D64, cfg.iters, cfg.l, cfg.q, lambda k: omega(cfg.seed, k, cfg.n, cfg.l).numpy(),
+                           rp=cfg.rp, norm2=n2, L0=L0, rho=cfg.params["rho"])
+    h, L, E, resid = _run_gpu(P, cfg, D, n2, cfg.iters, rho=cfg.params["rho"])
+    Lg = np64(L)
+    assert abs(np.linalg.norm(Lg - L0) / np.linalg.norm(L0) - ref["hist"]["nrmse"][-1]) <= 1e-3
+    assert np.linalg.norm(Lg - ref["L"]) <= 1e-3 * np.linalg.norm(ref["L"])
+    assert np.linalg.norm(np64(E) - ref["E"]) <= 1e-3 * np.linalg.norm(ref["E"])
