@@ -27,14 +27,16 @@
 // into gridDim.x contiguous ranges, one per CTA (stream-K): every SM streams
 // the same number of chunks, no wave tail. A range covering a whole tile
 // writes it directly; a tile split between CTAs leaves partial sums in a
-// per-CTA slot (first or last segment of the range) that tc_fixup_kernel adds
-// in CTA order (deterministic).
+// per-CTA slot (first or last segment of the range), and the CTA that
+// finishes a split tile last (per-tile arrival counter) adds all its slots in
+// CTA order (deterministic; tc_fixup_kernel does it after the pass when the
+// counters are disabled). Small K (the l x l applies): whole tiles per CTA.
 //
-// Roles per CTA (640 threads):
-//   warp 0      TMA producer of A (16 KB chunks, 9-deep ring, released as soon as
+// Roles per CTA (640 threads; 2-CTA clusters multicast the B stages):
+//   warp 0      TMA producer of A (16 KB chunks, 4-deep ring, released as soon as
 //               the converters hold the values in registers)
-//   warp 3      TMA producer of B_h (tf32, 128B swizzle) + B_l (bf16, 64B
-//               swizzle), 3-deep ring released by the MMA
+//   warp 3      TMA producer of B_h (tf32) + B_x (bf16 [b_l | b_h]), both
+//               128B swizzle, 5-deep ring released by the MMAs of both CTAs
 //   warp 1      MMA issuer (one thread); A operands from TMEM, B from smem
 //   warp 2      TMEM allocator
 //   warps 4..11 converters, two groups of four (one warp per TMEM lane
