@@ -616,7 +616,7 @@ frsvt_status chol2(frsvt_handle* h, T* Tout) {
   int* ok = h->lwd;
   unsigned long long* emax = (unsigned long long*)(h->lwd + 2);
   CK(cudaMemsetAsync(emax, 0, sizeof(unsigned long long), h->st));
-  const dim3 g((unsigned)cdiv(l, 32), (unsigned)cdiv(l, 32));
+  const dim3 g((unsigned)cdiv(l, LWD_T), (unsigned)cdiv(l, LWD_T));
   lowdin_sq_kernel<<<g, LWD_THREADS, lowdin_smem_bytes(l), h->st>>>(h->G, l, h->E2b, emax);
   TRY(post_launch(h));
   lowdin_series_kernel<T><<<g, LWD_THREADS, lowdin_smem_bytes(l), h->st>>>(h->G, h->E2b, l, emax, ok, Tout);
@@ -669,8 +669,8 @@ frsvt_status gram_fast(frsvt_handle* h, const T* Y, int64_t rows, bool sharded) 
 template <typename Tout>
 frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, int tb, Tout* C) {
   const int l = h->l;
-  const dim3 g((unsigned)cdiv(l, 32), (unsigned)cdiv(l, 32));
-  sgemm64_kernel<Tout><<<g, LWD_THREADS, (size_t)64 * l * sizeof(double), h->st>>>(l, l, l, A, l, ta, B, l, tb, C, l);
+  const dim3 g((unsigned)cdiv(l, LWD_T), (unsigned)cdiv(l, LWD_T));
+  sgemm64_kernel<Tout><<<g, LWD_THREADS, (size_t)2 * LWD_T * l * sizeof(double), h->st>>>(l, l, l, A, l, ta, B, l, tb, C, l);
   return post_launch(h);
 }
 
