@@ -428,7 +428,7 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
   const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
   const int64_t kx = cdiv(Ktot, tc::BK) * 2 * tc::BK;  // rows of the bf16 [b_l | b_h] operand
-  tc::split_tf32_bf16x2_kernel<<<dim3((unsigned)cdiv(kx / 2, 256), (unsigned)h->l), 256, 0, h->st>>>(
+  tc::split_tf32_bf16x2_kernel<<<dim3((unsigned)cdiv(kx / 2, 512), (unsigned)h->l), 256, 0, h->st>>>(
       B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
   TRY(post_launch(h));
   CUtensorMap mA, mBh, mBl;

@@ -668,24 +668,39 @@ __global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int N
 // B operand split: Bh = rna_tf32(x) (fp32, rows x cols, ld ldh) and Bx (bf16,
 // (2 * roundup32(rows)) x cols, ld ldx): for K chunk c, Bx rows 64c + j hold
 // bf16(x - Bh) at K = 32c + j (j < 32) and bf16(Bh) at K = 32c + j - 32
-// (j >= 32), zero past `rows`. One thread per (row, column), writing both halves.
+// (j >= 32), zero past `rows`. One thread per two rows of a column, writing both halves.
 __global__ void __launch_bounds__(256) split_tf32_bf16x2_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
                                                                   int64_t ldx_in, float* __restrict__ Bh, int64_t ldh,
                                                                   __nv_bfloat16* __restrict__ Bx, int64_t ldx) {
-  // grid (chunks of 256 rows, cols): thread = one row k of column j
+  // grid (chunks of 512 rows, cols): thread = rows k, k + 1 of column j
+  // (packed bf16x2 / float2 stores; X, Bh column starts are 8-byte aligned
+  // when ldx_in, ldh are even, else the scalar path)
   const int j = blockIdx.y;
-  const int64_t k = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t k = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
   const int64_t kpad = ((rows + 31) / 32) * 32;
   if (k >= kpad) return;
-  float x = 0.f, h = 0.f;
-  if (k < rows) {
-    x = X[k + j * ldx_in];
-    h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-    Bh[k + j * ldh] = h;
+  float x0 = 0.f, x1 = 0.f;
+  const float* xc = X + j * ldx_in;
+  if (k + 1 < rows && ((ldx_in | ldh) & 1) == 0) {
+    const float2 v = *reinterpret_cast<const float2*>(xc + k);
+    x0 = v.x;
+    x1 = v.y;
+  } else {
+    if (k < rows) x0 = xc[k];
+    if (k + 1 < rows) x1 = xc[k + 1];
   }
-  const int64_t base = (k >> 5) * 64 + (k & 31) + j * ldx;
-  Bx[base] = __float2bfloat16_rn(x - h);
-  Bx[base + 32] = __float2bfloat16_rn(h);
+  const float h0 = k < rows ? __uint_as_float((__float_as_uint(x0) + 0x1000u) & 0xFFFFE000u) : 0.f;
+  const float h1 = k + 1 < rows ? __uint_as_float((__float_as_uint(x1) + 0x1000u) & 0xFFFFE000u) : 0.f;
+  float* bh = Bh + j * ldh;
+  if (k + 1 < rows && ((ldx_in | ldh) & 1) == 0) {
+    *reinterpret_cast<float2*>(bh + k) = make_float2(h0, h1);
+  } else {
+    if (k < rows) bh[k] = h0;
+    if (k + 1 < rows) bh[k + 1] = h1;
+  }
+  const int64_t base = (k >> 5) * 64 + (k & 31) + j * ldx;  // k even: (k, k+1) in the same 32-chunk
+  *reinterpret_cast<__nv_bfloat162*>(Bx + base) = __floats2bfloat162_rn(x0 - h0, x1 - h1);
+  *reinterpret_cast<__nv_bfloat162*>(Bx + base + 32) = __floats2bfloat162_rn(h0, h1);
 }
 
 }  // namespace tc
