@@ -464,10 +464,16 @@ bool tc_small_ok(const frsvt_handle* h, int64_t rows) {
 frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const float* D, float* A, float* E,
                         int64_t ld, double rho, double lambda, int* nparts, bool fs_next = false) {
   const int Kp = h->Kp;
+  // compose2 (the iALM epilogue) splits Q~ itself while moving it to TMEM
+  const bool tma_ok = (ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0;
+  const bool use2 = h->cmp2 && epi != tc::EPI_STORE && tma_ok && (h->m % 4) == 0;
   {
-    dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
-    tc::split_transpose_kernel<<<g1, 256, 0, h->st>>>((const float*)h->Qt, h->m, h->l, h->m, Kp, h->QtTh, h->QtTl);
-    TRY(post_launch(h));
+    if (!use2) {
+      dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
+      tc::split_transpose_kernel<<<g1, 256, 0, h->st>>>((const float*)h->Qt, h->m, h->l, h->m, Kp, h->QtTh,
+                                                         h->QtTl);
+      TRY(post_launch(h));
+    }
     dim3 g2((unsigned)cdiv(h->n, 32), (unsigned)(Kp / 32));
     tc::split_transpose_kernel<<<g2, 256, 0, h->st>>>((const float*)h->Wt, h->n, h->l, h->n, Kp, h->WtTh, h->WtTl);
     TRY(post_launch(h));
@@ -493,10 +499,11 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   if (sp > ntiles) sp = ntiles;
   if (sp < 1) sp = 1;
   dim3 grid((unsigned)(nfull + rem * sp));
-  // compose2 streams D, A, E through TMA: 16-byte aligned columns required
-  const bool tma_ok = (ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0;
-  if (h->cmp2 && epi != tc::EPI_STORE && tma_ok) {
-    CUtensorMap mD, mA, mE;
+  // compose2 streams D, A, E through TMA: 16-byte aligned columns required (use2)
+  if (use2) {
+    CUtensorMap mD, mA, mE, mQ;
+    if (!make_map(&mQ, (const float*)h->Qt, h->m, h->l, h->m, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return FRSVT_ECUDA;
     if (!make_map(&mD, D, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mE, E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mA, epi == tc::EPI_ALM ? A : E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -520,7 +527,7 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
       attr2[EPIV][FSV] = true;                                                                                  \
     }                                                                                                           \
     tc::tc_compose2_kernel<EPIV, FSV><<<grid, tc::CMP_THREADS, smem2, h->st>>>(                                 \
-        mQh, mQl, mWh, mWl, mD, mA, mE, mOm, (int)h->m, (int)h->n, h->l, &h->dev->r, nfull, sp, X, ldx, A, E, \
+        mQ, mWh, mWl, mD, mA, mE, mOm, (int)h->m, (int)h->n, h->l, &h->dev->r, nfull, sp, X, ldx, A, E, \
         ld, h->dev->mu, rho, lambda, h->redpart, h->fspart, &h->dev->fs_done);                                  \
   } while (0)
     if (epi == tc::EPI_ALM && fs) FRSVT_LAUNCH_CMP2(tc::EPI_ALM, true);

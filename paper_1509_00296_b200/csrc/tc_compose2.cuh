@@ -11,7 +11,8 @@
 // 12-stage TMA ring of 8-column D/A/E slices (144 KB in flight per SM).
 //
 // Roles (640 threads):
-//   warp 0     TMA: the Q~ block (hi/lo, once, into the ring area), then Wt
+//   warp 0     TMA: the Q~ block (once, into the ring area; split into
+//              hi/lo by the epilogue warps on its way to TMEM), then Wt
 //              K-chunks of every column tile through a 2-stage ring
 //   warp 1     MMA: 3xTF32 with A = Q~ from TMEM, B = Wt from shared memory
 //   warp 2     TMEM allocator (512 columns)
@@ -73,8 +74,7 @@ struct Compose2Smem {
 // by fs_finish_kernel); *fs_done says whether it was formed.
 template <int EPI, bool FS>
 __global__ void __launch_bounds__(CMP_THREADS, 1)
-tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_constant__ CUtensorMap mapQl,
-                   const __grid_constant__ CUtensorMap mapWh, const __grid_constant__ CUtensorMap mapWl,
+tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapWh, const __grid_constant__ CUtensorMap mapWl,
                    const __grid_constant__ CUtensorMap mapD, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapE, const __grid_constant__ CUtensorMap mapOm, int m, int n,
                    int l, const int* __restrict__ r_dev, int nfull, int sp, float* __restrict__ X, int64_t ldx,
@@ -149,16 +149,13 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
 
   if (warp == 0) {
     if (lane == 0) {
-      prefetch_tmap(&mapQh);
-      prefetch_tmap(&mapQl);
+      prefetch_tmap(&mapQ);
       prefetch_tmap(&mapWh);
       prefetch_tmap(&mapWl);
       if (nk > 0) {
-        mbar_expect_tx(qfull, 2 * CB * nk);
-        for (int kc = 0; kc < nk; ++kc) {
-          tma_load_2d(ring + kc * CB, &mapQh, qfull, kc * BK, rb * 128);
-          tma_load_2d(ring + (4 + kc) * CB, &mapQl, qfull, kc * BK, rb * 128);
-        }
+        // Q~ (m x l column-major): K-chunk kc = box {128 rows, 32 columns}, column-major in smem
+        mbar_expect_tx(qfull, CB * nk);
+        for (int kc = 0; kc < nk; ++kc) tma_load_2d(ring + kc * CB, &mapQ, qfull, rb * 128, kc * BK);
         const uint64_t wpol = l2_policy_evict_last();  // Wt tiles are re-read by every row block
         int it = 0;
         for (int jt = jt0; jt < jt1; ++jt) {
@@ -232,23 +229,25 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQh, const __grid_const
     const int rloc = wq * 32 + lane;
     const int row = rb * 128 + rloc;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    // Q~ (hi/lo) of this row: staging (128B-swizzled K-major chunks) -> TMEM
+    // Q~ of this row: staging (column-major chunks) -> split into tf32 hi and
+    // the fp32 remainder lo (the 3xTF32 A operands) -> TMEM
     if (grp == 0 && nk > 0) {
       mbar_wait(qfull, 0);
 #pragma unroll 1
-      for (int q = 0; q < 2 * nk; ++q) {
-        const int hl = q & 1, kc = q >> 1;
-        const uint32_t a_s = smem_u32(ring + (hl * 4 + kc) * CB);
+      for (int kc = 0; kc < nk; ++kc) {
+        const float* qs = reinterpret_cast<const float*>(ring + kc * CB);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          uint32_t x[16];
+          uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int cc = 4 * half + c;
-            lds_u32x4(a_s + (uint32_t)(rloc * 128 + ((cc ^ (rloc & 7)) * 16)), x[4 * c], x[4 * c + 1], x[4 * c + 2],
-                      x[4 * c + 3]);
+          for (int c = 0; c < 16; ++c) {
+            const float x = qs[(16 * half + c) * 128 + rloc];
+            const uint32_t hx = rna_tf32(x);
+            hi[c] = hx;
+            lo[c] = __float_as_uint(x - __uint_as_float(hx));
           }
-          tmem_st16((hl ? t_ql : t_qh) + (uint32_t)(kc * BK + 16 * half) + lane_off, x);
+          tmem_st16(t_qh + (uint32_t)(kc * BK + 16 * half) + lane_off, hi);
+          tmem_st16(t_ql + (uint32_t)(kc * BK + 16 * half) + lane_off, lo);
         }
       }
       tc_wait_st();
