@@ -646,8 +646,12 @@ frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldi
 template <typename T>
 frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, const T* Msm, T* Out) {
   if constexpr (sizeof(T) == 4) {
-    if (tc_small_ok(h, rows))
+    if (tc_small_ok(h, rows)) {
+      if (h->pass2)  // stream-K pass with K = l: whole tiles per CTA pair
+        return tc_pass2<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out,
+                                     rows, nullptr, 0);
       return tc_AX_gen(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows, nullptr, 0);
+    }
   }
   return apply_small<T>(h, In, rows, rows, Msm, Out, rows);
 }
