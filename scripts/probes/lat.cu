@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/probes/lat scripts/probes/lat.cu
 // Latency probes (one warp unless noted): dependent DFMA chain, DMUL, fp64
 // division, MUFU rcp + Newton, mbarrier arrive -> wait ping-pong between two
 // warps, __syncthreads with 1024 threads.
