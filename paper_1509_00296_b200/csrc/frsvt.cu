@@ -1,13 +1,15 @@
 // libfrsvt: C ABI + orchestration of the FRSVT hot path on one B200 rank.
 // Declarations, argument meaning and error behaviour: include/frsvt.h.
 //
-// One call of frsvt_apply* / rpca_alm_step enqueues, on the handle's stream:
-//   omega -> Y = A Omega' (+ Q~)                          sketch   (Alg. 1 l.3-11)
-//   orth(Y) = CholeskyQR2 (fp64 Gram, pivoted Cholesky)     rank reveal
-//   q x { Z = orth(A^T Q); Y = A Z; Q = orth(Y) }           power iteration (l.13-15)
-//   B^T = A^T Q; G = B B^T (fp64); Jacobi -> U_B, sigma     small SVD (l.16-18)
-//   shrink -> Mc, Mp; Q~ = Q Mc; Wt = B^T Mp                Eq. (6) factors
-//   X = Q~ Wt^T  (or the fused iALM epilogue)               composition (l.19)
+// One call of frsvt_apply* / rpca_alm_step enqueues, on the handle's stream
+// (no host synchronisation, no allocation: a whole solve is graph-capturable):
+//   omega -> Y = [Q~, A Omega_p]                              sketch   (Alg. 1 l.3-11)
+//   orth(Y): fp64 Gram, Cholesky with column drop + explicit   rank reveal;
+//     factor (chol_inv), applied on tensor cores; with a carry  RP: fresh block only (R13)
+//   q x { Z = orth(A^T Q); Y = A Z; Q = orth2(Y) }              power iteration (l.13-15)
+//   B^T = A^T Q; G = B B^T (fp64); Jacobi -> U_B, sigma         small SVD (l.16-18; R16)
+//   shrink -> Mc, Mp; Q~ = Q Mc; Wt = B^T Mp                    Eq. (6) factors
+//   X = Q~ Wt^T  (or the fused iALM epilogue, compose2)         composition (l.19)
 // Row-sharded operands are reduced over ranks with NCCL where the contraction
 // runs over rows (Grams of m-row matrices, A^T Q, residual, init norms).
 #include "../../include/frsvt.h"
