@@ -581,7 +581,7 @@ template <typename T>
 frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded, const int* r_dev = nullptr) {
   const int l = h->l;
   if (h->dmma_gram) {  // fp64 tensor cores, upper 8x8 blocks only (gram_dmma.cuh)
-    // one wave (1 CTA of 256 threads per SM at ~250 registers), >= 32 rows each
+    // one wave (1 CTA of 512 threads per SM at 128 registers), >= 32 rows each
     int S = (int)cdiv(rows, GD_ROWS);
     const int Smax = (int)(h->partd_elems / ((size_t)l * l));
     if (S > h->nsm) S = h->nsm;

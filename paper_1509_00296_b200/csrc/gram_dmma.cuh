@@ -5,7 +5,7 @@
 // accumulated in fp64 by mma.sync.m8n8k4.f64 (DMMA): G is tiled into 8 x 8
 // blocks and only the upper-triangular ones are computed (symmetry halves the
 // work). Each CTA takes a contiguous range of rows, stages 32-row chunks in
-// shared memory (coalesced column reads), and its 8 warps own disjoint sets
+// shared memory (coalesced column reads), and its 16 warps own disjoint sets
 // of 8 x 8 blocks, accumulating in registers; one fp64 partial per CTA (both
 // triangles written), summed over CTAs by splitk_reduce_wide_kernel.
 #pragma once
@@ -13,10 +13,11 @@
 
 namespace frsvt {
 
-constexpr int GD_THREADS = 256;
+constexpr int GD_THREADS = 512;
 constexpr int GD_ROWS = 32;                 // rows per staged chunk
 constexpr int GD_LD = FRSVT_LMAX + 4;       // padded row stride (doubles) of the staged chunk
-constexpr int GD_MAXB = 17;                 // 8x8 blocks per warp: 16*17/2 = 136 for l = 128 over 8 warps
+constexpr int GD_WARPS = GD_THREADS / 32;
+constexpr int GD_MAXB = 9;                  // 8x8 blocks per warp: 16*17/2 = 136 for l = 128 over 16 warps
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -36,12 +37,12 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
   const int nb8 = (l + 7) >> 3;
   const int nblk = nb8 * (nb8 + 1) / 2;
   const int jb0 = r_dev ? (min(max(*r_dev, 0), l) >> 3) : 0;
-  // this warp's blocks: q = warp + 8 t, (bi <= bj) in row-major upper order
+  // this warp's blocks: q = warp + GD_WARPS t, (bi <= bj) in row-major upper order
   int bi[GD_MAXB], bj[GD_MAXB];
   double acc0[GD_MAXB], acc1[GD_MAXB];
 #pragma unroll
   for (int t = 0; t < GD_MAXB; ++t) {
-    int q = warp + 8 * t, i = 0;
+    int q = warp + GD_WARPS * t, i = 0;
     if (q < nblk) {
       while (q >= nb8 - i) {
         q -= nb8 - i;
@@ -62,7 +63,7 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
   const int kq = lane & 3, g = lane >> 2;
   // software pipeline: the next 32-row chunk is loaded into registers while
   // the current one is multiplied (all of a thread's loads in flight at once)
-  constexpr int PER = GD_ROWS * FRSVT_LMAX / GD_THREADS;  // 16 elements per thread
+  constexpr int PER = GD_ROWS * FRSVT_LMAX / GD_THREADS;  // 8 elements per thread
   Tin pre[PER];
   auto load_chunk = [&](int64_t rc) {
 #pragma unroll
