@@ -9,6 +9,9 @@ timeout 300 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gp
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${T}_ncu_launch.log 2>&1; echo ncu1=$? >> gpurun_out/${T}_status.txt
 timeout 300 python scripts/rpca_c5_steps.py 24 > gpurun_out/${T}_plain.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"tc_compose2_kernel|tc_pass2_kernel|eig_jacobi|gram_dmma|chol_inv" -s 60 -c 8 -o gpurun_out/${T}_prof \
+  -k regex:"tc_compose2_kernel" -s 18 -c 1 -o gpurun_out/${T}_prof_compose \
+  python scripts/rpca_c5_steps.py 24 > gpurun_out/${T}_ncu_full_compose.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k regex:"tc_pass2_kernel|eig_jacobi|gram_dmma|chol_inv" -s 60 -c 8 -o gpurun_out/${T}_prof \
   python scripts/rpca_c5_steps.py 24 > gpurun_out/${T}_ncu_full.log 2>&1; echo ncu2=$? >> gpurun_out/${T}_status.txt
 cat gpurun_out/${T}_status.txt
