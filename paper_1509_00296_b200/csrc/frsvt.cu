@@ -81,6 +81,7 @@ struct frsvt_handle {
   int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
   int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
   int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
+  int narrow_sketch; // 1: 32-column pass instance for the RP sketch when p <= 32 (FRSVT_NARROW)
   int warm_eig;      // 1: warm-started small SVD under range propagation (eig_warm.cuh, FRSVT_WARM_EIG)
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
   double ew_rot, ew_stop;  // fresh-block solve tolerances (the full solve refines)
@@ -366,12 +367,22 @@ frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q
   return tc_AtQ_gen(h, A, lda, h->m, h->n, Q, h->m, part, splits);
 }
 
+// flags[0] = (p > thr), flags[1] = (p <= thr) for p = l - *r_dev (the skip
+// flags of the two sketch instances)
+__global__ void sketch_width_kernel(const int* __restrict__ r_dev, int l, int thr, int* __restrict__ flags) {
+  if (threadIdx.x == 0) {
+    const int p = l - min(max(*r_dev, 0), l);
+    flags[0] = p > thr ? 1 : 0;
+    flags[1] = p > thr ? 0 : 1;
+  }
+}
+
 // ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
 template <int MODE, int NP, int CL>
 frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
                           const int* rp_dev, const int* skip_dev = nullptr) {
-  const size_t smem = tc::Pass2Smem::total(CL > 1 ? 128 : h->l);
+  const size_t smem = tc::Pass2Smem::total(CL > 1 ? NP : h->l, tc::p2_astages(NP));
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(tc::tc_pass2_kernel<MODE, NP, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -425,7 +436,10 @@ frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
 template <int MODE>
 frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
                       int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
-                      const int* rp_dev = nullptr, const int* skip_dev = nullptr) {
+                      const int* rp_dev = nullptr, const int* skip_dev = nullptr, int np_force = 0) {
+  // np_force: N tile of the instance (0: by l); a narrower instance multiplies
+  // only the first np_force columns of B (the RP sketch when p is small)
+  const int np = np_force ? np_force : tc_np(h->l);
   float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
   __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
   const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
@@ -434,7 +448,7 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
       B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
   TRY(post_launch(h));
   CUtensorMap mA, mBh, mBl;
-  const uint32_t nb = h->p2cl == 2 ? 64u : (uint32_t)h->l;  // clustered: each CTA loads a 64-row half
+  const uint32_t nb = h->p2cl == 2 ? (uint32_t)np / 2 : (uint32_t)h->l;  // clustered: each CTA loads an np/2-row half
   bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
                                   : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -448,7 +462,6 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   if (!ok) return FRSVT_ECUDA;
-  const int np = tc_np(h->l);
   if (np == 32)
     return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
   if (np == 64)
@@ -843,8 +856,23 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
       // (dev->fs_done); such a launch is not counted in the pass profile
       const int* skip = (h->fs_armed && ov == nullptr) ? &h->dev->fs_done : nullptr;
       if (!skip) TRY(prof_begin(h));
-      TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y, h->m,
-                                (const float*)h->Qt, h->m, 0, &h->dev->r, skip));
+      if (h->l > 32 && !skip && h->narrow_sketch) {
+        // p = l - r is known only on the device: both the full-width and the
+        // 32-column instance are enqueued, each skips unless it is the one
+        // for this p (flags[0]: p > 32, flags[1]: p <= 32); the carried
+        // columns are copied first (the narrow instance writes the fresh ones)
+        int* flags = h->lwd + 8;
+        sketch_width_kernel<<<1, 32, 0, h->st>>>(&h->dev->r, h->l, 32, flags);
+        TRY(post_launch(h));
+        CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
+        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, nullptr, 0, 0, &h->dev->r, flags + 1));
+        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, nullptr, 0, 0, &h->dev->r, flags, 32));
+      } else {
+        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, (const float*)h->Qt, h->m, 0, &h->dev->r, skip));
+      }
       if (!skip) TRY(prof_end(h, 0, (double)h->m * h->n * sizeof(T)));
     }
   }
@@ -1300,6 +1328,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     }
     const char* e8 = getenv("FRSVT_CMP2");
     h->cmp2 = !(e8 && e8[0] == '0');
+    const char* e14 = getenv("FRSVT_NARROW");
+    h->narrow_sketch = !(e14 && e14[0] == '0');
     const char* e9 = getenv("FRSVT_FS");  // opt-in: +0.5-1% iter/s on c5, at the cost of a slower composition
     h->fs = (e9 && e9[0] == '1');
     h->fs_armed = false;

@@ -60,6 +60,8 @@ namespace tc {
 #define P2_BST 5
 #endif
 constexpr int P2_ASTAGES = P2_AST;  // A ring (16 KB stages; released by the converters; even)
+// the A ring of an NP-column instance: the narrow (NP <= 32) B stages leave room for 8 stages
+__host__ __device__ constexpr int p2_astages(int np) { return np <= 32 ? 8 : P2_ASTAGES; }
 // B ring: released by the MMA. Its depth must cover MMA completion (~700
 // cycles) + the L2 latency of the small operand under the A stream (~1900
 // cycles, clock64 stamps): 5 stages of (roundup8(l) rows x 256 B)
@@ -76,8 +78,8 @@ struct Pass2Smem {
   static constexpr uint32_t b_bytes = bh_bytes + bx_bytes;    // 32 KB
   // one B stage for nb valid rows (128B-swizzle atoms are 8 rows = 1 KB)
   __host__ __device__ static constexpr uint32_t b_stage(int nb) { return 2u * (uint32_t)((nb + 7) / 8) * 1024u; }
-  __host__ __device__ static constexpr size_t total(int nb) {
-    return 1024 + (size_t)P2_ASTAGES * a_bytes + (size_t)P2_BSTAGES * b_stage(nb) + 512;
+  __host__ __device__ static constexpr size_t total(int nb, int ast = P2_ASTAGES) {
+    return 1024 + (size_t)ast * a_bytes + (size_t)P2_BSTAGES * b_stage(nb) + 512;
   }
 };
 
@@ -219,17 +221,18 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   // dbg (test hook only, 0 in production): bit 0 no MMA, bit 1 no conversion, bit 2 no B loads,
   // bit 3 no bf16 MMAs, bit 4 no a_lo MMAs, bit 5 clock64 stamps of CTA 0 into out (output invalid)
   static_assert(NP % 16 == 0 && NP >= 32 && NP <= 128, "N tile");
+  constexpr int AST = p2_astages(NP);
   constexpr uint32_t A_BYTES = Pass2Smem::a_bytes;
-  const uint32_t B_BYTES = Pass2Smem::b_stage(CL > 1 ? 128 : nbrows);  // Bh | Bx, each rows x 128 B
+  const uint32_t B_BYTES = Pass2Smem::b_stage(CL > 1 ? NP : nbrows);  // Bh | Bx, each rows x 128 B
   const uint32_t BHB = B_BYTES / 2;
   constexpr int HALF = NP / 2;  // columns per flush warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = smem;                                   // P2_ASTAGES x 16 KB
-  uint8_t* sB = smem + P2_ASTAGES * A_BYTES;            // P2_BSTAGES x B_BYTES
+  uint8_t* sA = smem;                                   // AST x 16 KB
+  uint8_t* sB = smem + AST * A_BYTES;            // P2_BSTAGES x B_BYTES
   uint64_t* fulla = (uint64_t*)(sB + P2_BSTAGES * B_BYTES);
-  uint64_t* emptya = fulla + P2_ASTAGES;
-  uint64_t* fullb = emptya + P2_ASTAGES;
+  uint64_t* emptya = fulla + AST;
+  uint64_t* fullb = emptya + AST;
   uint64_t* emptyb = fullb + P2_BSTAGES;
   uint64_t* tfull = emptyb + P2_BSTAGES;
   uint64_t* tempty = tfull + P2_TSTAGES;
@@ -258,11 +261,11 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int nloc = (int)(g1 - g0);
   // expected TMA bytes per B stage (CL = 1: boxes of nbrows rows; CL = 2: both
   // CTAs' 64-row halves, out-of-bounds rows zero-filled and counted)
-  const uint32_t brows = CL > 1 ? 128u : (uint32_t)nbrows;
+  const uint32_t brows = CL > 1 ? (uint32_t)NP : (uint32_t)nbrows;
   const uint32_t btx = brows * BK * 4u + brows * 2 * BK * 2u;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < P2_ASTAGES; ++s) {
+    for (int s = 0; s < AST; ++s) {
       mbar_init(&fulla[s], 1);
       mbar_init(&emptya[s], 4);
     }
@@ -301,8 +304,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
         const int64_t g = g0 + i;
         const int grp = (int)(g / nch), kc = (int)(g - (int64_t)grp * nch) * BK;
         const int tile = grp * CL + crank;
-        const int s = i % P2_ASTAGES;
-        const uint32_t ph = (i / P2_ASTAGES) & 1;
+        const int s = i % AST;
+        const uint32_t ph = (i / AST) & 1;
         mbar_wait(&emptya[s], ph ^ 1);
         p2_stamp(dbg, out, 0, i, nloc);
         mbar_expect_tx(&fulla[s], A_BYTES);
@@ -331,10 +334,10 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           continue;
         }
         mbar_expect_tx(&fullb[s], btx);
-        if (CL > 1) {  // my 64-row half of the stage, into both CTAs
-          const uint32_t ho = (uint32_t)crank * 64u * 128u;
-          tma_load_2d_mc(sB + s * B_BYTES + ho, &mapBh, &fullb[s], kc, 64 * crank, 0x3, pol);
-          tma_load_2d_mc(sB + s * B_BYTES + BHB + ho, &mapBl, &fullb[s], 2 * kc, 64 * crank, 0x3, pol);
+        if (CL > 1) {  // my NP/2-row half of the stage, into both CTAs
+          const uint32_t ho = (uint32_t)crank * (uint32_t)(NP / 2) * 128u;
+          tma_load_2d_mc(sB + s * B_BYTES + ho, &mapBh, &fullb[s], kc, (NP / 2) * crank, 0x3, pol);
+          tma_load_2d_mc(sB + s * B_BYTES + BHB + ho, &mapBl, &fullb[s], 2 * kc, (NP / 2) * crank, 0x3, pol);
         } else {
           tma_load_2d_hint(sB + s * B_BYTES, &mapBh, &fullb[s], kc, 0, pol);
           tma_load_2d_hint(sB + s * B_BYTES + BHB, &mapBl, &fullb[s], 2 * kc, 0, pol);
@@ -420,8 +423,8 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     for (int i = grp; i < nloc; i += 2) {
-      const int s = i % P2_ASTAGES;
-      const uint32_t ph = (i / P2_ASTAGES) & 1;
+      const int s = i % AST;
+      const uint32_t ph = (i / AST) & 1;
       const int t = i % P2_TSTAGES;
       const uint32_t tph = (i / P2_TSTAGES) & 1;
       mbar_wait(&fulla[s], ph);
