@@ -5,8 +5,8 @@
 // nearly aligned with the singular directions of B (their Gram block G_cc is
 // nearly diagonal and G_cf is small), while the p fresh columns are a random
 // basis of the rest: G_ff is a dense p x p block. The one-sided Jacobi then
-// spends its sweeps resolving G_ff. Diagonalising G_ff first (a 32-column
-// Jacobi on [[G_ff, 0], [0, c I]], c > lambda_max(G_ff)) and rotating G by
+// spends its sweeps resolving G_ff. Diagonalising G_ff first (a 24- or
+// 32-column Jacobi on [[G_ff, 0], [0, c I]], c > lambda_max(G_ff)) and rotating G by
 // V = blockdiag(I_r, V_f) leaves a nearly diagonal G2 = V^T G V, which the
 // full solve resolves in a few sweeps; U_B = V U2. Same eigenvalues, same
 // invariant subspaces (an exact similarity), so X is unchanged up to rounding.
@@ -19,14 +19,20 @@ namespace frsvt {
 
 constexpr int EW_P = 32;  // largest fresh block handled
 
-// Gpad (32 x 32, column-major) = [[G_ff, 0], [0, c I]]; *flag = 1 when the
-// warm start applies
+// Gpad (W x W, column-major) = [[G_ff, 0], [0, c I]], W = 24 when p <= 24
+// else 32 (fewer Jacobi rounds for the usual small p); flags[0] = W (0 when
+// the warm start does not apply), flags[1] = (W == 24), flags[2] = (W == 32)
 __global__ void __launch_bounds__(256) eig_fresh_pack_kernel(const double* __restrict__ G, int l,
                                                               const int* __restrict__ r_dev, double* __restrict__ Gpad,
-                                                              int* __restrict__ flag) {
+                                                              int* __restrict__ flags) {
   const int r = min(max(*r_dev, 0), l), p = l - r;
   const bool on = r > 0 && p >= 2 && p <= EW_P;
-  if (threadIdx.x == 0) *flag = on ? 1 : 0;
+  const int W = !on ? 0 : (p <= 24 ? 24 : EW_P);
+  if (threadIdx.x == 0) {
+    flags[0] = W;
+    flags[1] = W == 24 ? 1 : 0;
+    flags[2] = W == EW_P ? 1 : 0;
+  }
   if (!on) return;
   __shared__ double tr;
   if (threadIdx.x == 0) {
@@ -35,8 +41,8 @@ __global__ void __launch_bounds__(256) eig_fresh_pack_kernel(const double* __res
     tr = 2.0 * t + 1.0;  // > lambda_max(G_ff) (G_ff is PSD: lambda_max <= trace)
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < EW_P * EW_P; idx += blockDim.x) {
-    const int i = idx % EW_P, j = idx / EW_P;
+  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
+    const int i = idx % W, j = idx / W;
     double v = 0.0;
     if (i < p && j < p) v = G[(r + i) + (size_t)(r + j) * l];
     else if (i == j) v = tr;
@@ -44,20 +50,21 @@ __global__ void __launch_bounds__(256) eig_fresh_pack_kernel(const double* __res
   }
 }
 
-// G2 = V^T G V, V = blockdiag(I_r, V_f), V_f = Uf[0:p, 32-p:32] (the padding
-// eigenvalue c sorts first); a copy of G when the warm start is off
+// G2 = V^T G V, V = blockdiag(I_r, V_f), V_f = Uf[0:p, W-p:W] (the padding
+// eigenvalue c sorts first; Uf is W x W); a copy of G when the warm start is off
 __global__ void __launch_bounds__(256) eig_fresh_rotate_kernel(const double* __restrict__ G, int l,
                                                                 const int* __restrict__ r_dev,
                                                                 const double* __restrict__ Uf,
                                                                 const int* __restrict__ flag,
                                                                 double* __restrict__ G2) {
   __shared__ double Vf[EW_P * EW_P];
-  const bool on = *flag != 0;
+  const int W = *flag;
+  const bool on = W != 0;
   const int r = min(max(*r_dev, 0), l), p = l - r;
   if (on) {
     for (int idx = threadIdx.x; idx < EW_P * EW_P; idx += blockDim.x) {
       const int i = idx % EW_P, j = idx / EW_P;  // Vf[i + j * 32]
-      Vf[idx] = (i < p && j < p) ? Uf[i + (size_t)(EW_P - p + j) * EW_P] : 0.0;
+      Vf[idx] = (i < p && j < p) ? Uf[i + (size_t)(W - p + j) * W] : 0.0;
     }
   }
   __syncthreads();
@@ -88,12 +95,13 @@ __global__ void __launch_bounds__(128) eig_fresh_back_kernel(double* __restrict_
                                                               const int* __restrict__ r_dev,
                                                               const double* __restrict__ Uf,
                                                               const int* __restrict__ flag) {
-  if (!*flag) return;
+  const int W = *flag;
+  if (!W) return;
   const int r = min(max(*r_dev, 0), l), p = l - r;
   __shared__ double Vf[EW_P * EW_P];
   for (int idx = threadIdx.x; idx < EW_P * EW_P; idx += blockDim.x) {
     const int i = idx % EW_P, j = idx / EW_P;
-    Vf[idx] = (i < p && j < p) ? Uf[i + (size_t)(EW_P - p + j) * EW_P] : 0.0;
+    Vf[idx] = (i < p && j < p) ? Uf[i + (size_t)(W - p + j) * W] : 0.0;
   }
   __syncthreads();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;

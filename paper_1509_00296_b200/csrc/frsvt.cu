@@ -952,15 +952,19 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
   }
   if (h->warm_eig && h->rp != 0) {
     // warm start (R16): diagonalise the fresh block first, solve the rotated Gram
-    int* flag = h->lwd + 6;
+    int* flag = h->lwd + 12;  // [W, W == 24, W == 32] (lwd: [0..3] Loewdin, 4 debug, 7 sweeps scratch, 8..9 sketch)
     eig_fresh_pack_kernel<<<1, 256, 0, h->st>>>(h->G, h->l, &h->dev->r, h->ewbuf, flag);
     TRY(post_launch(h));
     double* Gpad = h->ewbuf;
     double* Uf = Gpad + EW_P * EW_P;
     double* sigf = Uf + EW_P * EW_P;
     double* G2 = sigf + EW_P;
+    // the fresh-block solve at width 24 or 32 (whichever the device-side p selected)
+    eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(24), EigJacobi::smem_bytes(24), h->st>>>(
+        Gpad, 24, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 1);
+    TRY(post_launch(h));
     eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(EW_P), EigJacobi::smem_bytes(EW_P), h->st>>>(
-        Gpad, EW_P, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag);
+        Gpad, EW_P, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 2);
     TRY(post_launch(h));
     eig_fresh_rotate_kernel<<<(unsigned)cdiv((int64_t)h->l * h->l, 256), 256, 0, h->st>>>(h->G, h->l, &h->dev->r,
                                                                                           Uf, flag, G2);
