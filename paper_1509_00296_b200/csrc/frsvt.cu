@@ -734,7 +734,17 @@ frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Ou
   chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, l, r_dev, 1e-12, (float*)h->T1, l,
                                                                           &h->dev->s, &h->dev->flags, nullptr);
   TRY(post_launch(h));
-  // r_dev: in place (Out == In): only the fresh columns are written
+  // r_dev: in place (Out == In): only the fresh columns are written; with
+  // p <= 32 on the 32-column instance (the device-side choice of R11)
+  if (r_dev && l > 32 && h->narrow_sketch) {
+    int* flags = h->lwd + 8;
+    sketch_width_kernel<<<1, 32, 0, h->st>>>(r_dev, l, 32, flags);
+    TRY(post_launch(h));
+    TRY(tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev,
+                              flags + 1));
+    return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev,
+                                 flags, 32);
+  }
   return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev);
 }
 
