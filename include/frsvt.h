@@ -71,7 +71,12 @@ typedef struct {
   int32_t nranks;           /* 1 for a single GPU */
   int32_t rank;             /* 0 .. nranks-1 */
   const unsigned char* nccl_id; /* host, 128 bytes from frsvt_get_unique_id on rank 0; NULL if nranks == 1 */
+  uint32_t options;         /* FRSVT_OPT_* bits (0 = defaults) */
 } frsvt_config;
+
+/* frsvt_config.options bits */
+#define FRSVT_OPT_FUSED_SKETCH 1u /* rpca_alm_step: form the next call's fresh sketch in the fused
+                                     epilogue (see rpca_alm_step); fp32, range propagation, one rank */
 
 /* Host-side report of one call (filling it synchronises the stream). */
 typedef struct {
@@ -93,7 +98,12 @@ frsvt_status frsvt_get_unique_id(unsigned char out[128]);
 
 /* Validate cfg, allocate every workspace for width l on the current device,
  * bind the work to `cuda_stream` (a cudaStream_t, NULL = legacy default),
- * and initialise NCCL when nranks > 1. *out is NULL on failure. */
+ * and initialise NCCL when nranks > 1 (collective over the ranks: the
+ * m_local-dependent route of the orthonormalisation is agreed there, so every
+ * rank takes the same one). *out is NULL on failure.
+ * Multi-rank fp32 handles additionally require, on every call, a 16-byte
+ * aligned operand with leading dimension % 4 == 0 (the tensor-core route must
+ * be the same on all ranks); otherwise the call returns FRSVT_EINVAL. */
 frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_handle** out);
 void frsvt_destroy(frsvt_handle* h);
 const char* frsvt_status_string(frsvt_status s);
@@ -134,8 +144,8 @@ frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda,
  * mu_0 (mu0, else 1.25/||D||_2), E_1, A_1. finalize != 0 writes L_{k+1} into
  * st->L and leaves D, E, A, mu untouched (the textbook state after k+1 steps).
  * D, E, A, L: m_local x n, leading dim ld. rel_resid: host, nullable (syncs).
- * Fused next sketch (opt-in, FRSVT_FS=1; fp32 tensor path, range propagation,
- * one rank): when p = l - r <= 24 the epilogue also forms the next call's
+ * Fused next sketch (opt-in, FRSVT_OPT_FUSED_SKETCH; fp32 tensor path, range
+ * propagation, one rank): when p = l - r <= 24 the epilogue also forms the next call's
  * fresh sketch A_{k+1} Omega_p and the next step skips that
  * pass. The contents of A (library-managed) must therefore not be changed by
  * the caller between consecutive steps unless a state setter runs in between
@@ -176,26 +186,25 @@ frsvt_status rpca_set_mu(frsvt_handle* h, double mu, double mu_bar);
 /* Number of kernels this handle has launched since creation (host counter). */
 int64_t frsvt_kernel_launches(const frsvt_handle* h);
 
-/* Test hook: one streaming pass with a chosen implementation (synchronises).
+/* Test hook: one streaming pass on a chosen route (synchronises).
  * kind 0: out (m_local x l, ld m_local) = A (m_local x n) * B (n x l, ld n)
  * kind 1: out (n x l, ld n) = A^T * B (m_local x l, ld m_local), summed over ranks
- * impl 0 = SIMT CUDA cores, 1 = tcgen05 3xTF32, 2 = persistent stream-K tcgen05
- * (fp32 handles; needs lda % 4 == 0 and a 16-byte aligned A, otherwise the
- * SIMT path runs). */
+ * impl 0 = SIMT CUDA cores, 2 = the persistent stream-K tcgen05 pass of the
+ * product path (fp32 handles; needs lda % 4 == 0 and a 16-byte aligned A,
+ * else FRSVT_EINVAL). */
 frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                               const void* B, void* out);
 /* Same pass `reps` times back to back on the handle's stream (no host sync
- * in between), *ms = mean device time per pass (CUDA events). impl as above;
- * impl 2 is the persistent stream-K pass, 3..5 and 8..71 are bandwidth and
- * pipeline probes of it (outputs not meaningful). Synchronises. */
+ * in between), *ms = mean device time per pass (CUDA events). impl as above,
+ * plus 8..135: the stream-K pass with parts of its pipeline switched off
+ * (bit field impl - 8, see tc_pass2.cuh; outputs not meaningful). Synchronises. */
 frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                                     const void* B, void* out, int32_t reps, double* ms);
 
 /* Test hook: the small SVD (Alg. 1 lines 16-18, reading Z8) alone, on an
  * l x l fp64 Gram G = B B^T (device, column-major, ld l; NULL = the Gram the
- * handle's last call decomposed). impl 0 is the production kernel (one-sided
- * Jacobi on G), 1 a two-sided Jacobi, 2 pivoted Cholesky + one-sided Jacobi
- * on the factor (earlier kernels, kept for comparison). Gcopy (device, nullable) receives the
+ * handle's last call decomposed). impl must be 0 (the production kernel:
+ * one-sided Jacobi on G). Gcopy (device, nullable) receives the
  * Gram used. Outputs: sigma (device, l values, descending), UB (device, l x l,
  * ld l), *sweeps (host, nullable) and, when reps > 0, the mean device time of
  * `reps` back-to-back launches (*ms, host). Synchronises. */

@@ -13,11 +13,11 @@ import os
 
 import torch
 
-from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FrsvtConfig, FrsvtInfo, RpcaState,
-                   load_library, status_string)
+from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, FrsvtConfig, FrsvtInfo,
+                   RpcaState, load_library, status_string)
 
 __all__ = ["Frsvt", "FrsvtError", "lib", "library_path", "colmajor", "W_EXPLICIT",
-           "W_RECIPROCAL", "W_REWEIGHTED"]
+           "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH"]
 
 W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
 
@@ -59,7 +59,7 @@ class Frsvt:
     iterations q, range propagation flag, dtype (torch.float32/float64)."""
 
     def __init__(self, m, n, l, q=1, rp=True, dtype=torch.float32, seed=0, stream=None,
-                 nranks=1, rank=0, m_global=None, row0=0, nccl_id=None, device=None):
+                 nranks=1, rank=0, m_global=None, row0=0, nccl_id=None, device=None, options=0):
         if device is not None:
             torch.cuda.set_device(device)
         self.m, self.n, self.l, self.q, self.rp = int(m), int(n), int(l), int(q), bool(rp)
@@ -77,6 +77,7 @@ class Frsvt:
         cfg.seed = int(seed)
         cfg.nranks = int(nranks)
         cfg.rank = int(rank)
+        cfg.options = int(options)
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = (ctypes.c_ubyte * 128)(*bytes(nccl_id))

@@ -24,7 +24,9 @@ class FrsvtConfig(ctypes.Structure):
                 ("m_global", ctypes.c_int64), ("row0", ctypes.c_int64), ("l", ctypes.c_int32),
                 ("q", ctypes.c_int32), ("range_propagation", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("nccl_id", ctypes.POINTER(ctypes.c_ubyte))]
+                ("nccl_id", ctypes.POINTER(ctypes.c_ubyte)), ("options", ctypes.c_uint32)]
+
+FRSVT_OPT_FUSED_SKETCH = 1
 
 
 class FrsvtInfo(ctypes.Structure):

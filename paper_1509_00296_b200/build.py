@@ -31,19 +31,36 @@ def nvcc_cmd(out=LIB, extra=()):
             *extra]
 
 
-def needs_build():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+STAMP = LIB + ".sha256"
+
+
+def source_digest():
+    """sha256 over the library's sources and the compile command: a prebuilt
+    .so is reused only if it was built from exactly these bytes."""
+    import hashlib
+    hsh = hashlib.sha256()
     deps = [os.path.join(ROOT, "include", "frsvt.h")]
-    for d in (os.path.join(HERE, "csrc"),):
-        deps += [os.path.join(d, f) for f in os.listdir(d)]
-    return any(os.path.getmtime(p) > t for p in deps)
+    csrc = os.path.join(HERE, "csrc")
+    deps += sorted(os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh", ".h")))
+    for p in deps:
+        hsh.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as f:
+            hsh.update(f.read())
+    hsh.update(" ".join(nvcc_cmd()[:12]).encode())
+    return hsh.hexdigest()
+
+
+def needs_build():
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    with open(STAMP) as f:
+        return f.read().strip() != source_digest()
 
 
 def build(force=False, verbose=False):
     if not force and not needs_build():
         return LIB
+    digest = source_digest()
     cmd = nvcc_cmd()
     p = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
@@ -54,6 +71,8 @@ def build(force=False, verbose=False):
         raise RuntimeError("nvcc failed building libfrsvt.so (see %s)" % log)
     if verbose:
         sys.stderr.write(p.stderr)
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
     return LIB
 
 

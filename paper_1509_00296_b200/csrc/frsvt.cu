@@ -16,18 +16,17 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "small.cuh"
-#include "small2.cuh"
 #include "eig_jacobi.cuh"
 #include "eig_warm.cuh"
 #include "orth_chol.cuh"
 #include "lowdin.cuh"
-#include "chol_fast.cuh"
 #include "chol_inv.cuh"
 #include "gram_dmma.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
 #include "tc_pass2.cuh"
 #include "tc_compose2.cuh"
+#include "tc_pass3.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -75,30 +74,22 @@ struct frsvt_handle {
   float *QtTh, *QtTl, *WtTh, *WtTl;  // K-major (Kp x rows) splits for the composition
   int Kp;
   int64_t ldxs, ldqs;
-  int use_tc;
-  int pass2;         // 1: persistent stream-K passes (tc_pass2.cuh), 0: tc_pass_kernel
-  int p2cl;          // stream-K pass cluster size (1, or 2: B stages multicast to a CTA pair)
-  int dmma_gram;     // 1: fp64 Grams on the DMMA tensor cores (gram_dmma.cuh)
-  int infix;         // 1: stream-K fixup inside the pass kernel (per-tile counters)
-  int cmp2;          // 1: TMA-streamed iALM composition (tc_compose2.cuh) for EPI_ALM / EPI_FINAL
-  int narrow_sketch; // 1: 32-column pass instance for the RP sketch when p <= 32 (FRSVT_NARROW)
-  int warm_eig;      // 1: warm-started small SVD under range propagation (eig_warm.cuh, FRSVT_WARM_EIG)
+  int use_tc;        // fp32 handle with TMA available: tcgen05 passes (else SIMT, fp64 handles)
+  int tc_m;          // tensor-core small-operand path for the m-row matrices (Y, Q); rank-uniform
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
-  double ew_rot, ew_stop;  // fresh-block solve tolerances (the full solve refines)
-  int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_FS=1)
+  int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_OPT_FUSED_SKETCH)
   bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
   float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
   float* OmT;        // Omega^T, n x 24 (the fused sketch's TMA operand)
   size_t fspart_ctas;
   unsigned int* tilecnt;  // per-tile arrival counters (zero between passes)
   int ncnt;
-  int lowdin;        // 1: second CholeskyQR pass by the Loewdin series when it converges
   double* E2b;       // Loewdin workspace E^2 (l x l fp64)
   double* Rf;        // first-pass CholeskyQR factor R' (l x l row-major fp64)
-  int fastchol;      // fp32 orth1: 4 chol_inv + tensor apply (default), 1 R + row TRSM, 2/3 T + tensor apply, 0 SIMT
   double *T2d, *Hd, *McD, *MpD;  // fp64 l x l: pending second CholeskyQR factor and fold scratch
   int t2_pending;    // 1: h->Q holds Q1 and the basis is Q1 T2d (T2d folded into G, Mc, Mp)
-  int* lwd;          // device ints: [0] ok flag, [2..3] max|E| (u64)
+  int* lwd;          // device ints: [0] Loewdin ok, [2..3] max|E| (u64), [4] debug r, [6] create flag,
+                     // [7] fresh-block sweeps, [8..9] sketch-width flags, [12..14] fresh-block width flags
   int nsm;           // SMs of the device (stream-K grid)
   float* skpart;     // stream-K partial-tile slots (nsm x 2 x 128 x 128 fp32)
   __nv_bfloat16 *Xb, *Qb;  // bf16 [b_l | b_h] operands of the stream-K passes (ld ldb16)
@@ -304,12 +295,7 @@ template <int MODE, int NP>
 frsvt_status launch_tc_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, int splits, float* out, int64_t ldo, int64_t zstride,
                           const float* add, int64_t ldadd) {
-  const size_t smem = tc::PassSmem::total(NP);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(tc::tc_pass_kernel<MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  const size_t smem = tc::PassSmem::total(NP);  // attribute set in frsvt_create
   const int nchunks = (int)cdiv(Ktot, tc::BK);
   const int cps = (int)cdiv(nchunks, splits);
   dim3 grid((unsigned)cdiv(Mtot, 128), (unsigned)splits);
@@ -334,22 +320,6 @@ frsvt_status split_small(frsvt_handle* h, const float* X, int64_t rows, int64_t 
   return post_launch(h);
 }
 
-// Y (M x l, ldy) = A (M x K, lda) X (K x l, ldx) (+ Add) on tensor cores (3xTF32)
-frsvt_status tc_AX_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t M, int64_t K, const float* X,
-                       int64_t ldx, float* Y, int64_t ldy, const float* Add, int64_t ldadd) {
-  TRY(split_small(h, X, K, ldx, h->Xh, h->Xl, h->ldxs));
-  const uint32_t np = (uint32_t)tc_np(h->l);
-  CUtensorMap mA, mBh, mBl;
-  if (!make_map(&mA, A, M, K, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map(&mBh, h->Xh, K, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mBl, h->Xl, K, h->l, h->ldxs, tc::BK, np, CU_TENSOR_MAP_SWIZZLE_128B))
-    return FRSVT_ECUDA;
-  return launch_tc<tc::MODE_AX>(h, mA, mBh, mBl, (int)M, (int)K, 1, Y, ldy, 0, Add, ldadd);
-}
-frsvt_status tc_AX(frsvt_handle* h, const float* A, int64_t lda, const float* X, float* Y, const float* Add) {
-  return tc_AX_gen(h, A, lda, h->m, h->n, X, h->n, Y, h->m, Add, h->m);
-}
-
 // partials (splits x Mcols x l) of A^T Q, A (rows x Mcols, lda), Q (rows x l, ldq), split-K over rows
 frsvt_status tc_AtQ_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t rows, int64_t Mcols, const float* Q,
                         int64_t ldq, float* part, int splits) {
@@ -363,9 +333,6 @@ frsvt_status tc_AtQ_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t ro
   return launch_tc<tc::MODE_ATQ>(h, mA, mBh, mBl, (int)Mcols, (int)rows, splits, part, Mcols,
                                  (int64_t)Mcols * h->l, nullptr, 0);
 }
-frsvt_status tc_AtQ(frsvt_handle* h, const float* A, int64_t lda, const float* Q, float* part, int splits) {
-  return tc_AtQ_gen(h, A, lda, h->m, h->n, Q, h->m, part, splits);
-}
 
 // flags[0] = (p > thr), flags[1] = (p <= thr) for p = l - *r_dev (the skip
 // flags of the two sketch instances)
@@ -378,17 +345,15 @@ __global__ void sketch_width_kernel(const int* __restrict__ r_dev, int l, int th
 }
 
 // ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
-template <int MODE, int NP, int CL>
-frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
+// stream-K passes run on 2-CTA clusters (the B stages multicast to the pair)
+constexpr int P2_CL = 2;
+
+template <int MODE, int NP>
+frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
                           int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
                           const int* rp_dev, const int* skip_dev = nullptr) {
-  const size_t smem = tc::Pass2Smem::total(CL > 1 ? NP : h->l, tc::p2_astages(NP));
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(tc::tc_pass2_kernel<MODE, NP, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)tc::Pass2Smem::total(FRSVT_LMAX)));
-    attr_set = true;
-  }
+  constexpr int CL = P2_CL;
+  const size_t smem = tc::Pass2Smem::total(NP, tc::p2_astages(NP));  // attribute set in frsvt_create
   const int mtiles = (int)cdiv(Mtot, 128);
   const int64_t mgroups = cdiv(mtiles, CL);
   const int64_t total = mgroups * cdiv(Ktot, tc::BK);
@@ -411,24 +376,11 @@ frsvt_status launch_p2_cl(frsvt_handle* h, const CUtensorMap& mA, const CUtensor
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  unsigned int* cnt = (h->infix && mtiles <= h->ncnt && !(dbg & 96)) ? h->tilecnt : nullptr;
+  if (mtiles > h->ncnt) return FRSVT_EINVAL;  // the tile counters cover every row tile (sized at create)
   CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
-                        ldadd, h->skpart, rp_dev, dbg, cnt, skip_dev));
-  TRY(post_launch(h));
-  if ((dbg & 96) || cnt || talign) return FRSVT_OK;
-  // one block per (tile, 8-column group): enough independent loads in flight
-  tc::tc_fixup_kernel<NP, CL><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, 8)), 256, 0, h->st>>>(
-      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev);
+                        ldadd, h->skpart, rp_dev, dbg, h->tilecnt, skip_dev));
+  (void)G;
   return post_launch(h);
-}
-
-template <int MODE, int NP>
-frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
-                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
-                          const int* rp_dev = nullptr, const int* skip_dev = nullptr) {
-  if (h->p2cl == 2)
-    return launch_p2_cl<MODE, NP, 2>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
-  return launch_p2_cl<MODE, NP, 1>(h, mA, mBh, mBl, Mtot, Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
 }
 
 // out (Mtot x l) = op(A) * B, B (Ktot x l, ld ldb) the small operand:
@@ -448,7 +400,7 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
       B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
   TRY(post_launch(h));
   CUtensorMap mA, mBh, mBl;
-  const uint32_t nb = h->p2cl == 2 ? (uint32_t)np / 2 : (uint32_t)h->l;  // clustered: each CTA loads an np/2-row half
+  const uint32_t nb = (uint32_t)np / 2;  // each CTA of the pair loads an np/2-row half of a B stage
   bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
                                   : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -469,9 +421,106 @@ frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
   return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
 }
 
-// tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows) matrix
-bool tc_small_ok(const frsvt_handle* h, int64_t rows) {
+// ---- CTA-pair (cta_group::2) stream-K passes (tc_pass3.cuh) -----------------
+template <int MODE, int NP, int TERMS>
+frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBx,
+                       int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
+                       const int* rp_dev, const int* skip_dev) {
+  constexpr int CL = 2;
+  const size_t smem = tc::Pass3Smem::total(NP, TERMS);  // attribute set in frsvt_create
+  const int mtiles = (int)cdiv(Mtot, 128);
+  const int64_t mgroups = cdiv(mtiles, CL);
+  const int64_t total = mgroups * cdiv(Ktot, tc::BK);
+  const int Gmax = h->nsm / CL;
+  // small K (the l x l applies of the orthonormalisation): whole tiles per
+  // cluster, no split tiles (dbg bit 8)
+  const bool talign = Ktot <= 8 * tc::BK;
+  if (talign) dbg |= 256;
+  const int64_t units = talign ? mgroups : total;
+  const int G = (int)(units < Gmax ? units : Gmax);
+  if (mtiles > h->ncnt) return FRSVT_EINVAL;  // the tile counters cover every row tile (sized at create)
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(G * CL));
+  lc.blockDim = dim3(tc::P3_THREADS);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&lc, tc::tc_pass3_kernel<MODE, NP, TERMS>, mA, mBh, mBx, Mtot, Ktot, h->l, out, ldo, add,
+                        ldadd, h->skpart, rp_dev, dbg, h->tilecnt, skip_dev));
+  return post_launch(h);
+}
+
+// out (Mtot x l) = op(A) * B on CTA pairs, B (Ktot x l, ld ldb) the small
+// operand: MODE_AX: A is Mtot x Ktot (lda); MODE_ATQ: A is Ktot x Mtot (lda),
+// op = ^T. terms 3: fp32-level product; terms 2: product with the
+// tf32-rounded B (span-only passes, reading R17).
+template <int MODE>
+frsvt_status tc_pass3(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
+                      int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int terms, int dbg = 0,
+                      const int* rp_dev = nullptr, const int* skip_dev = nullptr, int np_force = 0) {
+  const int np = np_force ? np_force : tc_np(h->l);
+  float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
+  __nv_bfloat16* Bx = MODE == tc::MODE_AX ? h->Xb : h->Qb;
+  const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
+  const int64_t kpad = cdiv(Ktot, tc::BK) * tc::BK;
+  const uint32_t nb = (uint32_t)np / 2;  // each CTA of the pair holds an np/2-row half of a B stage
+  CUtensorMap mA, mBh, mBx;
+  bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
+                                  : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (terms == 3) {
+    const int64_t kx = 2 * kpad;  // rows of the bf16 [b_l | b_h] operand
+    tc::split_tf32_bf16x2_kernel<<<dim3((unsigned)cdiv(kx / 2, 512), (unsigned)h->l), 256, 0, h->st>>>(
+        B, Ktot, h->l, ldb, Bh, ldh, Bx, h->ldb16);
+    TRY(post_launch(h));
+    cuuint64_t dims[2] = {(cuuint64_t)kx, (cuuint64_t)h->l};
+    cuuint64_t strides[1] = {(cuuint64_t)h->ldb16 * 2};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * tc::BK), nb};
+    cuuint32_t es[2] = {1, 1};
+    ok = ok && g_encode(&mBx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)Bx, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  } else {
+    tc::split_tf32_bf16_kernel<<<dim3((unsigned)cdiv(kpad / 2, 256), (unsigned)h->l), 256, 0, h->st>>>(
+        B, Ktot, ldb, Bh, ldh, Bx, kpad);
+    TRY(post_launch(h));
+    cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)h->l};
+    cuuint64_t strides[1] = {(cuuint64_t)kpad * 2};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, nb};
+    cuuint32_t es[2] = {1, 1};
+    ok = ok && g_encode(&mBx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)Bx, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!ok) return FRSVT_ECUDA;
+#define FRSVT_P3(NPV, TV) \
+  launch_p3<MODE, NPV, TV>(h, mA, mBh, mBx, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev)
+  if (terms == 3) {
+    if (np == 32) return FRSVT_P3(32, 3);
+    if (np == 64) return FRSVT_P3(64, 3);
+    return FRSVT_P3(128, 3);
+  }
+  if (np == 32) return FRSVT_P3(32, 2);
+  if (np == 64) return FRSVT_P3(64, 2);
+  return FRSVT_P3(128, 2);
+#undef FRSVT_P3
+}
+
+// tensor-core path for the small-operand GEMMs of a (rows x l, ld = rows)
+// matrix. For the row-sharded m-row matrices (m_rows) the choice was made once
+// in frsvt_create and agreed over the ranks (h->tc_m): every rank must take the
+// same orthonormalisation route, or the replicated factors would differ.
+bool tc_small_local(const frsvt_handle* h, int64_t rows) {
   return h->use_tc && h->esz == 4 && h->l >= 16 && (rows % 4) == 0 && rows >= 128;
+}
+bool tc_small_ok(const frsvt_handle* h, int64_t rows, bool m_rows) {
+  return m_rows ? h->tc_m != 0 : tc_small_local(h, rows);
 }
 
 // X = Q~ Wt^T fused with its consumer (tc::EPI_*) on tensor cores. Returns the
@@ -481,7 +530,7 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   const int Kp = h->Kp;
   // compose2 (the iALM epilogue) splits Q~ itself while moving it to TMEM
   const bool tma_ok = (ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0;
-  const bool use2 = h->cmp2 && epi != tc::EPI_STORE && tma_ok && (h->m % 4) == 0;
+  const bool use2 = epi != tc::EPI_STORE && tma_ok && (h->m % 4) == 0;
   {
     if (!use2) {
       dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
@@ -532,15 +581,9 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
       if (!make_map(&mOm, h->OmT, tc::FS_PMAX, h->n, tc::FS_PMAX, tc::FS_PMAX, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
         return FRSVT_ECUDA;
     }
-    const size_t smem2 = tc::Compose2Smem::total();
-    static bool attr2[3][2] = {{false, false}, {false, false}, {false, false}};
+    const size_t smem2 = tc::Compose2Smem::total();  // attributes set in frsvt_create
 #define FRSVT_LAUNCH_CMP2(EPIV, FSV)                                                                            \
   do {                                                                                                          \
-    if (!attr2[EPIV][FSV]) {                                                                                    \
-      CK(cudaFuncSetAttribute(tc::tc_compose2_kernel<EPIV, FSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                              (int)smem2));                                                                     \
-      attr2[EPIV][FSV] = true;                                                                                  \
-    }                                                                                                           \
     tc::tc_compose2_kernel<EPIV, FSV><<<grid, tc::CMP_THREADS, smem2, h->st>>>(                                 \
         mQ, mWh, mWl, mD, mA, mE, mOm, (int)h->m, (int)h->n, h->l, &h->dev->r, nfull, sp, X, ldx, A, E, \
         ld, h->dev->mu, rho, lambda, h->redpart, h->fspart, &h->dev->fs_done);                                  \
@@ -559,14 +602,9 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
     }
     return FRSVT_OK;
   }
-  const size_t smem = tc::ComposeSmem::total();
-  static bool attr[3] = {false, false, false};
+  const size_t smem = tc::ComposeSmem::total();  // attributes set in frsvt_create
 #define FRSVT_LAUNCH_CMP(EPIV)                                                                                  \
   do {                                                                                                          \
-    if (!attr[EPIV]) {                                                                                          \
-      CK(cudaFuncSetAttribute(tc::tc_compose_kernel<EPIV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      attr[EPIV] = true;                                                                                        \
-    }                                                                                                           \
     tc::tc_compose_kernel<EPIV><<<grid, tc::CMP_THREADS, smem, h->st>>>(mQh, mQl, mWh, mWl, (int)h->m, (int)h->n, \
                                                                         &h->dev->r, nfull, sp, X, ldx, D, A, E, ld,    \
                                                                         h->dev->mu, rho, lambda, h->redpart);    \
@@ -593,26 +631,17 @@ template <> ncclDataType_t nccl_type<double>() { return ncclFloat64; }
 template <typename T>
 frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sharded, const int* r_dev = nullptr) {
   const int l = h->l;
-  if (h->dmma_gram) {  // fp64 tensor cores, upper 8x8 blocks only (gram_dmma.cuh)
-    // one wave (1 CTA of 512 threads per SM at 128 registers), >= 32 rows each
-    int S = (int)cdiv(rows, GD_ROWS);
-    const int Smax = (int)(h->partd_elems / ((size_t)l * l));
-    if (S > h->nsm) S = h->nsm;
-    if (S > Smax) S = Smax;
-    if (S < 1) S = 1;
-    const int64_t rpc = cdiv(cdiv(rows, S), GD_ROWS) * GD_ROWS;
-    S = (int)cdiv(rows, rpc);
-    gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd, r_dev);
-    TRY(post_launch(h));
-    splitk_reduce_wide_kernel<double, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(h->partd, S, l,
-                                                                                                     l, h->G, l);
-    TRY(post_launch(h));
-    if (sharded) TRY(allreduce(h, h->G, (size_t)l * l, ncclFloat64, ncclSum));
-    return FRSVT_OK;
-  }
-  const int S = gram_splits(rows);
-  EpiStore<double> epi{h->partd, l, (int64_t)l * l};
-  TRY(launch_gram_tile<T>(h, l, (int)rows, S, Y, ld, epi));
+  // fp64 tensor cores (DMMA), upper 8x8 blocks only (gram_dmma.cuh); one wave
+  // (1 CTA of 512 threads per SM at 128 registers), >= 32 rows each
+  int S = (int)cdiv(rows, GD_ROWS);
+  const int Smax = (int)(h->partd_elems / ((size_t)l * l));
+  if (S > h->nsm) S = h->nsm;
+  if (S > Smax) S = Smax;
+  if (S < 1) S = 1;
+  const int64_t rpc = cdiv(cdiv(rows, S), GD_ROWS) * GD_ROWS;
+  S = (int)cdiv(rows, rpc);
+  gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd, r_dev);
+  TRY(post_launch(h));
   splitk_reduce_wide_kernel<double, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(h->partd, S, l, l,
                                                                                                    h->G, l);
   TRY(post_launch(h));
@@ -633,7 +662,6 @@ frsvt_status chol(frsvt_handle* h, T* Tout, const int* skip = nullptr) {
 // Loewdin series when max|G - I| <= 0.05, else the Cholesky kernel (lowdin.cuh)
 template <typename T>
 frsvt_status chol2(frsvt_handle* h, T* Tout) {
-  if (!h->lowdin) return chol<T>(h, Tout);
   const int l = h->l;
   int* ok = h->lwd;
   unsigned long long* emax = (unsigned long long*)(h->lwd + 2);
@@ -659,14 +687,11 @@ frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldi
 // Out = In * M with a well-conditioned M (orthogonal-like): tensor cores when
 // eligible (3xTF32, ~2e-6 relative), else SIMT
 template <typename T>
-frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, const T* Msm, T* Out) {
+frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, bool m_rows, const T* Msm, T* Out) {
   if constexpr (sizeof(T) == 4) {
-    if (tc_small_ok(h, rows)) {
-      if (h->pass2)  // stream-K pass with K = l: whole tiles per CTA pair
-        return tc_pass2<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out,
-                                     rows, nullptr, 0);
-      return tc_AX_gen(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows, nullptr, 0);
-    }
+    if (tc_small_ok(h, rows, m_rows))  // stream-K pass with K = l: whole tiles per CTA pair
+      return tc_pass2<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows,
+                                   nullptr, 0);
   }
   return apply_small<T>(h, In, rows, rows, Msm, Out, rows);
 }
@@ -674,9 +699,10 @@ frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, const T* Msm
 // G = Y^T Y of a nearly orthonormal Y (second CholeskyQR pass): tensor cores
 // when eligible (fp32 partials of 3xTF32 products, folded in fp64), else fp64 SIMT
 template <typename T>
-frsvt_status gram_fast(frsvt_handle* h, const T* Y, int64_t rows, bool sharded) {
+frsvt_status gram_fast(frsvt_handle* h, const T* Y, int64_t rows, bool m_rows) {
+  const bool sharded = m_rows && h->cfg.nranks > 1;
   if constexpr (sizeof(T) == 4) {
-    if (tc_small_ok(h, rows)) {
+    if (tc_small_ok(h, rows, m_rows)) {
       const int l = h->l;
       int S = (int)cdiv(rows, 256);
       if (S > 296) S = 296;
@@ -700,43 +726,20 @@ frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, 
   return post_launch(h);
 }
 
-// CholeskyQR, first pass (readings R2/R4 in DESIGN.md): fp64 Gram, Cholesky
-// with column drop, fp32-accurate apply. Out = Y T1 spans range(Y) and is
-// orthonormal up to ~u kappa(Y): enough wherever only the span of the basis
-// matters next (the next orthonormalisation follows: the sketch before a
-// power step, Z = A^T Q before A Z), so the second pass runs only on the
-// final basis of the range finder (orth_final).
-template <int NB>
-frsvt_status trsm_rows_nb(frsvt_handle* h, const float* In, int64_t rows, float* Out) {
-  const size_t smem = (size_t)(32 * NB) * (32 * NB + 1) * sizeof(float) + 16;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(trsm_rows_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  trsm_rows_kernel<NB><<<(unsigned)cdiv(rows, 128), 128, smem, h->st>>>(In, rows, rows, h->Rf, h->l, Out, rows);
-  return post_launch(h);
-}
-
 // CholeskyQR first pass with the explicit factor T of chol_inv_kernel (one
 // barrier per column, no triangular solve) applied by the stream-K tensor-core
 // pass. r_dev (range propagation, reading R11): In = [Q~ | Y_p]; only the
 // fresh block is factored and, in place (Out == In), Y_p <- (Y_p - Q~ Q~^T Y_p) T22.
-frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Out, bool sharded, const int* r_dev) {
+frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Out, bool m_rows, const int* r_dev) {
   const int l = h->l;
+  const bool sharded = m_rows && h->cfg.nranks > 1;
   TRY(gram<float>(h, In, rows, rows, sharded, r_dev));
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(chol_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)chol_inv_smem_bytes()));
-    attr = true;
-  }
   chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, l, r_dev, 1e-12, (float*)h->T1, l,
                                                                           &h->dev->s, &h->dev->flags, nullptr);
   TRY(post_launch(h));
   // r_dev: in place (Out == In): only the fresh columns are written; with
   // p <= 32 on the 32-column instance (the device-side choice of R11)
-  if (r_dev && l > 32 && h->narrow_sketch) {
+  if (r_dev && l > 32) {
     int* flags = h->lwd + 8;
     sketch_width_kernel<<<1, 32, 0, h->st>>>(r_dev, l, 32, flags);
     TRY(post_launch(h));
@@ -748,27 +751,16 @@ frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Ou
   return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev);
 }
 
+// CholeskyQR, first pass (readings R2/R4/R14 in DESIGN.md): fp64 Gram,
+// Cholesky with column drop and explicit factor, fp32-accurate apply. Out =
+// Y T1 spans range(Y) and is orthonormal up to ~u kappa(Y): enough wherever
+// only the span of the basis matters next (R9), so the second pass runs only
+// on the final basis of the range finder (orth_final).
 template <typename T>
-frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
+frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool m_rows) {
+  const bool sharded = m_rows && h->cfg.nranks > 1;
   if constexpr (sizeof(T) == 4) {
-    if (h->fastchol == 4 && h->pass2 && tc_small_ok(h, rows))
-      return orth1_inv(h, (const float*)In, rows, (float*)Out, sharded, nullptr);
-    if (h->fastchol == 2 || (h->fastchol == 3 && tc_small_ok(h, rows))) {
-      // Cholesky with explicit T, applied on tensor cores (tf32-level products
-      // as the SIMT fp32 apply: ~1e-6 of |Y||T|)
-      TRY(gram<T>(h, In, rows, rows, sharded));
-      TRY(chol<T>(h, (T*)h->T1));
-      return apply_fast<T>(h, In, rows, (const T*)h->T1, Out);
-    }
-    if (h->fastchol) {  // R' by the blocked Cholesky (no inverse), Q1 = Y R'^{-1} by row-parallel TRSM
-      TRY(gram<T>(h, In, rows, rows, sharded));
-      orth_chol_kernel<float><<<1, OC_THREADS, orth_chol_smem_bytes(h->l), h->st>>>(
-          h->G, h->l, 1e-12, (float*)nullptr, &h->dev->s, &h->dev->flags, nullptr, nullptr, h->Rf);
-      TRY(post_launch(h));
-      if (h->l <= 32) return trsm_rows_nb<1>(h, (const float*)In, rows, (float*)Out);
-      if (h->l <= 64) return trsm_rows_nb<2>(h, (const float*)In, rows, (float*)Out);
-      return trsm_rows_nb<4>(h, (const float*)In, rows, (float*)Out);
-    }
+    if (tc_small_ok(h, rows, m_rows)) return orth1_inv(h, (const float*)In, rows, (float*)Out, m_rows, nullptr);
   }
   TRY(gram<T>(h, In, rows, rows, sharded));
   TRY(chol<T>(h, (T*)h->T1));
@@ -780,9 +772,9 @@ frsvt_status orth1(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool shar
 // T2 is folded into the l x l factors downstream (t2_pending; small_svd,
 // shrink_and_factors): B^T = (A^T Q1) T2, Q~ = Q1 (T2 Mc), Wt = (A^T Q1) (T2 Mp).
 template <typename T>
-frsvt_status orth_final(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool sharded) {
-  TRY(orth1<T>(h, In, rows, Out, sharded));
-  TRY(gram_fast<T>(h, Out, rows, sharded));
+frsvt_status orth_final(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool m_rows) {
+  TRY(orth1<T>(h, In, rows, Out, m_rows));
+  TRY(gram_fast<T>(h, Out, rows, m_rows));
   TRY(chol2<double>(h, h->T2d));
   h->t2_pending = 1;
   return FRSVT_OK;
@@ -794,11 +786,8 @@ frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y,
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
-      if (h->pass2)
-        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)X, h->n, (float*)Y, h->m,
-                                  (const float*)Add, h->m));
-      else
-        TRY(tc_AX(h, (const float*)A, lda, (const float*)X, (float*)Y, (const float*)Add));
+      TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)X, h->n, (float*)Y, h->m,
+                                (const float*)Add, h->m));
       return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
     }
   }
@@ -816,29 +805,21 @@ frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y,
 // Z (n x l) = A^T (n x m) * Q (m x l), split-K over rows, all-reduced over ranks
 template <typename T>
 frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z) {
-  const int S = atq_splits(h->n, h->m, h->l);
-  EpiStore<T> epi{(T*)h->partq, h->n, (int64_t)h->n * h->l};
-  bool done = false;
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
-      if (h->pass2) {
-        TRY(tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)Q, h->m, (float*)Z, h->n,
-                                   nullptr, 0));
-        TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
-        TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
-        return FRSVT_OK;
-      }
-      TRY(tc_AtQ(h, (const float*)A, lda, (const float*)Q, (float*)h->partq, S));
+      TRY(tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)Q, h->m, (float*)Z, h->n,
+                                 nullptr, 0));
       TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
-      done = true;
+      TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
+      return FRSVT_OK;
     }
   }
-  if (!done) {
-    TRY(prof_begin(h));
-    TRY((launch_skinny<T, T, false, true>(h, (int)h->n, h->l, (int)h->m, S, A, lda, Q, h->m, nullptr, epi)));
-    TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
-  }
+  const int S = atq_splits(h->n, h->m, h->l);
+  EpiStore<T> epi{(T*)h->partq, h->n, (int64_t)h->n * h->l};
+  TRY(prof_begin(h));
+  TRY((launch_skinny<T, T, false, true>(h, (int)h->n, h->l, (int)h->m, S, A, lda, Q, h->m, nullptr, epi)));
+  TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
   splitk_reduce_kernel<T, T><<<grid1d(h->n * h->l), 256, 0, h->st>>>((const T*)h->partq, S, (int)h->n, h->l, Z, h->n);
   TRY(post_launch(h));
   TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
@@ -854,7 +835,7 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   // RP on the stream-K path: multiply only the p fresh columns (Alg. 1 RP
   // branch) and place them behind the carried Q~
   bool rp_front = false;
-  if constexpr (sizeof(T) == 4) rp_front = use_carry && h->pass2 && tc_eligible(h, A, lda);
+  if constexpr (sizeof(T) == 4) rp_front = use_carry && tc_eligible(h, A, lda);
   omega_kernel<T><<<grid1d(h->n * l), 256, 0, h->st>>>((T*)h->Om, h->n, l, &h->dev->r, use_carry ? 1 : 0,
                                                        h->cfg.seed, stream + (uint32_t)call, ov, h->n,
                                                        rp_front ? 1 : 0);
@@ -866,7 +847,7 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
       // (dev->fs_done); such a launch is not counted in the pass profile
       const int* skip = (h->fs_armed && ov == nullptr) ? &h->dev->fs_done : nullptr;
       if (!skip) TRY(prof_begin(h));
-      if (h->l > 32 && !skip && h->narrow_sketch) {
+      if (h->l > 32 && !skip) {
         // p = l - r is known only on the device: both the full-width and the
         // 32-column instance are enqueued, each skips unless it is the one
         // for this p (flags[0]: p > 32, flags[1]: p <= 32); the carried
@@ -888,38 +869,31 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   }
   h->fs_armed = false;
   if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
-  const bool sh = h->cfg.nranks > 1;
   h->t2_pending = 0;
-  if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh);
+  if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true);
   // with range propagation on the tensor path the sketch basis is formed in
   // place in Y: [Q~ | orth(Y_p - Q~ Q~^T Y_p)] (reading R11)
   const T* Qcur = (const T*)h->Q;
   bool rp_orth = false;
-  if constexpr (sizeof(T) == 4) rp_orth = rp_front && h->fastchol == 4 && h->pass2 && tc_small_ok(h, h->m);
+  if constexpr (sizeof(T) == 4) rp_orth = rp_front && tc_small_ok(h, h->m, true);
   if (rp_orth) {
-    if constexpr (sizeof(T) == 4) TRY(orth1_inv(h, (const float*)h->Y, h->m, (float*)h->Y, sh, &h->dev->r));
+    if constexpr (sizeof(T) == 4) TRY(orth1_inv(h, (const float*)h->Y, h->m, (float*)h->Y, true, &h->dev->r));
     Qcur = (const T*)h->Y;
   } else {
-    TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
+    TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
   }
   for (int it = 0; it < q; ++it) {
     TRY(gemm_AtQ<T>(h, A, lda, it == 0 ? Qcur : (const T*)h->Q, (T*)h->Z));
     TRY(orth1<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, false));
     TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr));
-    if (it + 1 < q) TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
-    else TRY(orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, sh));
+    if (it + 1 < q) TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
+    else TRY(orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
   }
   return FRSVT_OK;
 }
 
-size_t jacobi_eig_smem_bytes(int l) {
-  return ((size_t)l * (l + 1) / 2 + (size_t)l * l + FRSVT_LMAX) * sizeof(double) + 3 * (FRSVT_LMAX / 2) * sizeof(int);
-}
-
-// small SVD of the l x l fp64 Gram G (reading Z8). impl 0: production
-// (register-resident one-sided Jacobi on G, eig_jacobi.cuh); 1: two-sided
-// Jacobi reference; 2: pivoted Cholesky + one-sided Jacobi (small2.cuh);
-// t_mode 0: no shortcut, 1: scalar
+// small SVD of the l x l fp64 Gram G (reading Z8): register-resident
+// one-sided Jacobi on G (eig_jacobi.cuh); t_mode 0: no shortcut, 1: scalar
 // threshold t_host, 2: scalar threshold *t_dev (exact Gershgorin early-out).
 frsvt_status launch_eig_jacobi(frsvt_handle* h, const double* G, double* sigma, double* UB, int t_mode,
                                double t_host, const double* t_dev) {
@@ -935,21 +909,6 @@ frsvt_status launch_eig_jacobi(frsvt_handle* h, const double* G, double* sigma, 
   return post_launch(h);
 }
 
-frsvt_status launch_eig(frsvt_handle* h, int impl, const double* G, double* sigma, double* UB, int t_mode = 0,
-                        double t_host = 0.0, const double* t_dev = nullptr) {
-  const int l = h->l;
-  if (impl == 0) return launch_eig_jacobi(h, G, sigma, UB, t_mode, t_host, t_dev);
-  if (impl == 1) {
-    jacobi_eig_kernel<<<1, 1024, jacobi_eig_smem_bytes(l), h->st>>>(G, l, 40, sigma, UB, &h->dev->sweeps,
-                                                                   &h->dev->flags);
-    return post_launch(h);
-  }
-  const double jtol = h->esz == 8 ? 1e-15 : 1e-10;
-  small2_kernel<SM2_EIG, double><<<1, SM2_THREADS, small2_smem_bytes(l, SM2_EIG), h->st>>>(
-      G, l, 4e-15, nullptr, sigma, UB, &h->dev->s2, &h->dev->sweeps, &h->dev->flags, 40, jtol);
-  return post_launch(h);
-}
-
 // B^T = A^T Q, G = B B^T, Jacobi -> sigma, U_B   (Alg. 1 lines 16-18)
 template <typename T>
 frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0, double t_host = 0.0,
@@ -960,7 +919,7 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     TRY(gemm_ll<double>(h, h->G, 0, h->T2d, 0, h->Hd));
     TRY(gemm_ll<double>(h, h->T2d, 1, h->Hd, 0, h->G));
   }
-  if (h->warm_eig && h->rp != 0) {
+  if (h->rp != 0) {
     // warm start (R16): diagonalise the fresh block first, solve the rotated Gram
     int* flag = h->lwd + 12;  // [W, W == 24, W == 32] (lwd: [0..3] Loewdin, 4 debug, 7 sweeps scratch, 8..9 sketch)
     eig_fresh_pack_kernel<<<1, 256, 0, h->st>>>(h->G, h->l, &h->dev->r, h->ewbuf, flag);
@@ -969,21 +928,24 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     double* Uf = Gpad + EW_P * EW_P;
     double* sigf = Uf + EW_P * EW_P;
     double* G2 = sigf + EW_P;
+    // fresh-block solve tolerances: those of the main solve (R3; the full
+    // solve refines), fp64 handles to 1e-15
+    const double ew_rot = h->esz == 4 ? 1e-9 : 1e-15, ew_stop = h->esz == 4 ? 1e-4 : 0.0;
     // the fresh-block solve at width 24 or 32 (whichever the device-side p selected)
     eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(24), EigJacobi::smem_bytes(24), h->st>>>(
-        Gpad, 24, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 1);
+        Gpad, 24, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 1);
     TRY(post_launch(h));
     eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(EW_P), EigJacobi::smem_bytes(EW_P), h->st>>>(
-        Gpad, EW_P, nullptr, 0.0, 0, h->ew_rot, h->ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 2);
+        Gpad, EW_P, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 2);
     TRY(post_launch(h));
     eig_fresh_rotate_kernel<<<(unsigned)cdiv((int64_t)h->l * h->l, 256), 256, 0, h->st>>>(h->G, h->l, &h->dev->r,
                                                                                           Uf, flag, G2);
     TRY(post_launch(h));
-    TRY(launch_eig(h, 0, G2, h->sigma, h->UB, t_mode, t_host, t_dev));
+    TRY(launch_eig_jacobi(h, G2, h->sigma, h->UB, t_mode, t_host, t_dev));
     eig_fresh_back_kernel<<<(unsigned)cdiv(h->l, 128), 128, 0, h->st>>>(h->UB, h->l, &h->dev->r, Uf, flag);
     return post_launch(h);
   }
-  return launch_eig(h, 0, h->G, h->sigma, h->UB, t_mode, t_host, t_dev);
+  return launch_eig_jacobi(h, h->G, h->sigma, h->UB, t_mode, t_host, t_dev);
 }
 
 // shrink + factors: Q~ = Q Mc, Wt = B^T Mp (Eq. 6 with the kept set)
@@ -1004,8 +966,8 @@ frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const do
                                            &h->dev->r, &h->dev->flags, h->dev->rep);
     TRY(post_launch(h));
   }
-  TRY(apply_fast<T>(h, (const T*)h->Q, h->m, (const T*)h->Mc, (T*)h->Qt));
-  TRY(apply_fast<T>(h, (const T*)h->Z, h->n, (const T*)h->Mp, (T*)h->Wt));
+  TRY(apply_fast<T>(h, (const T*)h->Q, h->m, true, (const T*)h->Mc, (T*)h->Qt));
+  TRY(apply_fast<T>(h, (const T*)h->Z, h->n, false, (const T*)h->Mp, (T*)h->Wt));
   return FRSVT_OK;
 }
 
@@ -1131,7 +1093,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
       // fused next sketch: the next call's Omega and the carried columns of Y
       // are set up here; the composition forms Y_p when p = l - r <= FS_PMAX
       // (device-side decision) and the next sketch pass is then skipped
-      const bool fs_next = !finalize && h->fs && h->cmp2 && h->pass2 && h->rp != 0 && h->cfg.nranks == 1 &&
+      const bool fs_next = !finalize && h->fs && h->rp != 0 && h->cfg.nranks == 1 &&
                            tc_eligible(h, A, st->ld) && !h->override_pending;
       if (fs_next) {
         omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 1,
@@ -1165,31 +1127,62 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   return FRSVT_OK;
 }
 
-template <typename T>
-void set_smem_attrs() {
-  cudaFuncSetAttribute(orth_chol_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)orth_chol_smem_bytes(FRSVT_LMAX));
-}
-
-// streaming-rate probe of the pass partition (impl 3..5 of frsvt_debug_pass)
-template <int MODE, int SUB>
-frsvt_status probe_stream(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, float* sink) {
-  CUtensorMap mA;
-  const bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
-                                        : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!ok) return FRSVT_ECUDA;
-  const size_t smem = 1024 + (size_t)8 * 128 * tc::BK * 4 + 256;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(tc::tma_stream_probe_kernel<MODE, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    attr = true;
-  }
-  tc::tma_stream_probe_kernel<MODE, SUB><<<h->nsm, 64, smem, h->st>>>(mA, (int)Mtot, (int)Ktot, sink);
-  return post_launch(h);
+// dynamic shared-memory limits of every kernel that needs more than 48 KB,
+// set for the current device (attributes are per device; frsvt_create runs
+// this on the handle's device)
+frsvt_status set_smem_attrs() {
+#define FRSVT_ATTR(K, BYTES) CK(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BYTES)))
+  FRSVT_ATTR(orth_chol_kernel<float>, orth_chol_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(orth_chol_kernel<double>, orth_chol_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(sgemm64_kernel<float>, lowdin_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(sgemm64_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(lowdin_sq_kernel, lowdin_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(lowdin_series_kernel<float>, lowdin_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(lowdin_series_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(eig_jacobi_kernel, EigJacobi::smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(chol_inv_kernel<float>, chol_inv_smem_bytes());
+  FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 32>), tc::PassSmem::total(32));
+  FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 64>), tc::PassSmem::total(64));
+  FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 128>), tc::PassSmem::total(128));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 32, P2_CL>), tc::Pass2Smem::total(32, tc::p2_astages(32)));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 64, P2_CL>), tc::Pass2Smem::total(64, tc::p2_astages(64)));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 128, P2_CL>), tc::Pass2Smem::total(128, tc::p2_astages(128)));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 32, P2_CL>), tc::Pass2Smem::total(32, tc::p2_astages(32)));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 64, P2_CL>), tc::Pass2Smem::total(64, tc::p2_astages(64)));
+  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 128, P2_CL>), tc::Pass2Smem::total(128, tc::p2_astages(128)));
+#define FRSVT_ATTR3(MODE, NPV, TV) FRSVT_ATTR((tc::tc_pass3_kernel<MODE, NPV, TV>), tc::Pass3Smem::total(NPV, TV))
+  FRSVT_ATTR3(tc::MODE_AX, 32, 2);
+  FRSVT_ATTR3(tc::MODE_AX, 64, 2);
+  FRSVT_ATTR3(tc::MODE_AX, 128, 2);
+  FRSVT_ATTR3(tc::MODE_AX, 32, 3);
+  FRSVT_ATTR3(tc::MODE_AX, 64, 3);
+  FRSVT_ATTR3(tc::MODE_AX, 128, 3);
+  FRSVT_ATTR3(tc::MODE_ATQ, 32, 2);
+  FRSVT_ATTR3(tc::MODE_ATQ, 64, 2);
+  FRSVT_ATTR3(tc::MODE_ATQ, 128, 2);
+  FRSVT_ATTR3(tc::MODE_ATQ, 32, 3);
+  FRSVT_ATTR3(tc::MODE_ATQ, 64, 3);
+  FRSVT_ATTR3(tc::MODE_ATQ, 128, 3);
+#undef FRSVT_ATTR3
+  FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_ALM, false>), tc::Compose2Smem::total());
+  FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_ALM, true>), tc::Compose2Smem::total());
+  FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_FINAL, false>), tc::Compose2Smem::total());
+  FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_STORE>, tc::ComposeSmem::total());
+  FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_ALM>, tc::ComposeSmem::total());
+  FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_FINAL>, tc::ComposeSmem::total());
+#undef FRSVT_ATTR
+  return FRSVT_OK;
 }
 
 }  // namespace
+
+// Multi-rank handles: the pass route (tensor cores vs SIMT, and with it the
+// range-propagation bookkeeping) depends on the operand's alignment, so every
+// rank must see a TMA-compatible operand (16-byte aligned, ld % 4 == 0) on the
+// tensor path; anything else would make ranks build different bases.
+static bool rank_uniform_layout(const frsvt_handle* h, const void* A, int64_t lda) {
+  return h->cfg.nranks <= 1 || !h->use_tc || tc_eligible(h, A, lda);
+}
 
 // ============================================================== C ABI
 extern "C" {
@@ -1325,27 +1318,12 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
     if (nsm > 256) nsm = 256;  // stream-K fixup resolves <= 256 covering CTAs per tile
     h->nsm = nsm;
-    const char* e = getenv("FRSVT_PASS2");
-    h->pass2 = !(e && e[0] == '0');
-    const char* e11 = getenv("FRSVT_WARM_EIG");
-    h->warm_eig = !(e11 && e11[0] == '0');
-    // fresh-block solve: fp32 handles as the main solve (R3; the full solve
-    // refines), fp64 handles to 1e-15; FRSVT_EW_TOL="rot,stop" overrides
-    const char* e12 = getenv("FRSVT_EW_TOL");
-    h->ew_rot = c.dtype == FRSVT_F32 ? 1e-9 : 1e-15;
-    h->ew_stop = c.dtype == FRSVT_F32 ? 1e-4 : 0.0;
-    if (e12) sscanf(e12, "%lf,%lf", &h->ew_rot, &h->ew_stop);
     if (cudaMalloc((void**)&h->ewbuf, sizeof(double) * (2 * EW_P * EW_P + EW_P + (size_t)l * l)) != cudaSuccess) {
       cudaGetLastError();
       free_handle(h);
       return FRSVT_ENOMEM;
     }
-    const char* e8 = getenv("FRSVT_CMP2");
-    h->cmp2 = !(e8 && e8[0] == '0');
-    const char* e14 = getenv("FRSVT_NARROW");
-    h->narrow_sketch = !(e14 && e14[0] == '0');
-    const char* e9 = getenv("FRSVT_FS");  // opt-in: +0.5-1% iter/s on c5, at the cost of a slower composition
-    h->fs = (e9 && e9[0] == '1');
+    h->fs = (c.options & FRSVT_OPT_FUSED_SKETCH) ? 1 : 0;
     h->fs_armed = false;
     h->fspart_ctas = (size_t)cdiv(maxrows, 128) + 2 * (size_t)h->nsm + 8;
     if (cudaMalloc((void**)&h->fspart, sizeof(float) * tc::FS_PMAX * 128 * h->fspart_ctas) != cudaSuccess ||
@@ -1354,8 +1332,6 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
       free_handle(h);
       return FRSVT_ENOMEM;
     }
-    const char* e7 = getenv("FRSVT_INFIX");
-    h->infix = !(e7 && e7[0] == '0');
     h->ncnt = (int)cdiv(maxrows, 128) + 8;
     if (cudaMalloc((void**)&h->tilecnt, sizeof(unsigned int) * h->ncnt) != cudaSuccess ||
         cudaMemset(h->tilecnt, 0, sizeof(unsigned int) * h->ncnt) != cudaSuccess) {
@@ -1363,14 +1339,6 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
       free_handle(h);
       return FRSVT_ENOMEM;
     }
-    const char* e6 = getenv("FRSVT_DMMA_GRAM");
-    h->dmma_gram = !(e6 && e6[0] == '0');
-    const char* e5 = getenv("FRSVT_P2CL");
-    h->p2cl = (e5 && e5[0] == '1') ? 1 : 2;
-    const char* e3 = getenv("FRSVT_LOWDIN");
-    h->lowdin = !(e3 && e3[0] == '0');
-    const char* e4 = getenv("FRSVT_FASTCHOL");  // 0: T + SIMT apply, 1: R + TRSM, 2/3: T + tensor apply
-    h->fastchol = e4 ? (e4[0] - '0') : 4;
     if (c.dtype == FRSVT_F32 &&
         (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
@@ -1380,35 +1348,30 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
       return FRSVT_ENOMEM;
     }
   }
-  {
-    const char* e = getenv("FRSVT_SIMT");
-    h->use_tc = (c.dtype == FRSVT_F32) && !(e && e[0] == '1') && tma_encode_available();
-  }
+  h->use_tc = (c.dtype == FRSVT_F32) && tma_encode_available();
+  h->tc_m = tc_small_local(h, h->m) ? 1 : 0;
   cudaMemset(h->dev, 0, sizeof(DevState));
   cudaMemset(h->sigma, 0, sizeof(double) * FRSVT_LMAX);
   cudaMemset(h->dprev, 0, sizeof(double) * FRSVT_LMAX);
-  set_smem_attrs<float>();
-  set_smem_attrs<double>();
-  cudaFuncSetAttribute(small2_kernel<SM2_EIG, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)small2_smem_bytes(FRSVT_LMAX, SM2_EIG));
-  cudaFuncSetAttribute(sgemm64_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)lowdin_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(sgemm64_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)lowdin_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(lowdin_sq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)lowdin_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(lowdin_series_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)lowdin_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(lowdin_series_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)lowdin_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)jacobi_eig_smem_bytes(FRSVT_LMAX));
-  cudaFuncSetAttribute(eig_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)EigJacobi::smem_bytes(FRSVT_LMAX));
+  if (set_smem_attrs() != FRSVT_OK) {
+    free_handle(h);
+    return FRSVT_ECUDA;
+  }
   if (c.nranks > 1) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, 128);
     if (ncclCommInitRank(&h->comm, c.nranks, id, c.rank) != ncclSuccess) {
+      free_handle(h);
+      return FRSVT_ENCCL;
+    }
+    // rank-uniform path choices (the tensor-core orthonormalisation of the
+    // m-row matrices depends on m_local): agree on the minimum over ranks
+    int* flag = h->lwd + 6;
+    if (cudaMemcpyAsync(flag, &h->tc_m, sizeof(int), cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
+        ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, h->comm, h->st) != ncclSuccess ||
+        cudaMemcpyAsync(&h->tc_m, flag, sizeof(int), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
+        cudaStreamSynchronize(h->st) != cudaSuccess) {
+      cudaGetLastError();
       free_handle(h);
       return FRSVT_ENCCL;
     }
@@ -1432,6 +1395,7 @@ frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau
                          frsvt_info* info) {
   if (h) h->fs_armed = false;  // a fused next sketch belongs to rpca_alm_step
   if (!h || !A || !X || lda < h->m || ldx < h->m || !(tau >= 0) || !std::isfinite(tau)) return FRSVT_EINVAL;
+  if (!rank_uniform_layout(h, A, lda)) return FRSVT_EINVAL;
   if (h->cfg.dtype == FRSVT_F32) return apply_impl<float>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
   return apply_impl<double>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
 }
@@ -1441,6 +1405,7 @@ frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda, i
                                   frsvt_info* info) {
   if (h) h->fs_armed = false;
   if (!h || !A || !X || lda < h->m || ldx < h->m) return FRSVT_EINVAL;
+  if (!rank_uniform_layout(h, A, lda)) return FRSVT_EINVAL;
   int km;
   if (wmode == 0) {
     if (!w) return FRSVT_EINVAL;
@@ -1464,6 +1429,7 @@ frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, do
   if (st->iter < 0) return FRSVT_EINVAL;
   if (st->iter == 0 && !(st->mu_max_factor >= 1.0)) return FRSVT_EINVAL;
   if (st->norm2_D < 0 || st->mu0 < 0 || !std::isfinite(st->norm2_D) || !std::isfinite(st->mu0)) return FRSVT_EINVAL;
+  if (!rank_uniform_layout(h, st->A, st->ld) || !rank_uniform_layout(h, st->D, st->ld)) return FRSVT_EINVAL;
   if (h->cfg.dtype == FRSVT_F32) return rpca_impl<float>(h, st, finalize, rel_resid);
   return rpca_impl<double>(h, st, finalize, rel_resid);
 }
@@ -1559,42 +1525,29 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : 
 
 static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                                       const void* B, void* out) {
-  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 151) return FRSVT_EINVAL;
-  if (impl >= 8 && impl <= 135 && h->esz == 4 && tma_encode_available()) {  // pass2 with pipeline parts disabled
-    frsvt_status st = kind == 0 ? tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n,
-                                                       (float*)out, h->m, nullptr, 0, impl - 8)
-                                : tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m,
-                                                        (float*)out, h->n, nullptr, 0, impl - 8);
-    return st;
+  // impl 0: SIMT passes; 2: the stream-K tcgen05 pass; 8..135: the same pass
+  // with parts of its pipeline disabled (dbg = impl - 8, outputs invalid)
+  if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 263 || impl == 1 ||
+      (impl >= 5 && impl < 8))
+    return FRSVT_EINVAL;
+  if (impl >= 2 && !(h->esz == 4 && h->use_tc && tc_eligible(h, A, lda))) return FRSVT_EINVAL;
+  if (impl == 3 || impl == 4 || impl >= 136) {  // CTA-pair pass: 3 exact, 4 tf32-rounded B, 136.. probes
+    const int terms = impl == 4 ? 2 : 3;
+    const int dbg = impl >= 136 ? impl - 136 : 0;
+    return kind == 0 ? tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n, (float*)out,
+                                             h->m, nullptr, 0, terms, dbg)
+                     : tc_pass3<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m,
+                                              (float*)out, h->n, nullptr, 0, terms, dbg);
   }
-  if (impl == 150 || impl == 151) {  // fp64 rate probe: out[0] cycles, out[1] flops of CTA 0
-    fp64_rate_probe_kernel<<<h->nsm, 512, 0, h->st>>>(impl - 150, 4096, (float*)out);
-    return post_launch(h);
+  if (impl >= 2) {
+    const int dbg = impl >= 8 ? impl - 8 : 0;
+    return kind == 0 ? tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n, (float*)out,
+                                             h->m, nullptr, 0, dbg)
+                     : tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m, (float*)out,
+                                              h->n, nullptr, 0, dbg);
   }
-  if (impl >= 140 && impl <= 144 && h->esz == 4) {  // tensor-pipe rate probe, out[0] = cycles per MMA
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(tc::mma_rate_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-      attr = true;
-    }
-    tc::mma_rate_probe_kernel<<<h->nsm, 128, 80 * 1024, h->st>>>(impl - 140, 2000, (float*)out);
-    return post_launch(h);
-  }
-  if (impl >= 3 && h->esz == 4 && tma_encode_available()) {
-    const bool ax = kind == 0;
-    frsvt_status st;
-    if (impl == 3) st = ax ? probe_stream<tc::MODE_AX, 1>(h, (const float*)A, lda, h->m, h->n, (float*)out)
-                           : probe_stream<tc::MODE_ATQ, 1>(h, (const float*)A, lda, h->n, h->m, (float*)out);
-    else if (impl == 4) st = ax ? probe_stream<tc::MODE_AX, 2>(h, (const float*)A, lda, h->m, h->n, (float*)out)
-                                : probe_stream<tc::MODE_ATQ, 2>(h, (const float*)A, lda, h->n, h->m, (float*)out);
-    else st = ax ? probe_stream<tc::MODE_AX, 4>(h, (const float*)A, lda, h->m, h->n, (float*)out)
-                 : probe_stream<tc::MODE_ATQ, 4>(h, (const float*)A, lda, h->n, h->m, (float*)out);
-    return st;
-  }
-  const int saved = h->use_tc, saved2 = h->pass2;
-  if (impl >= 1 && !(h->esz == 4 && tma_encode_available())) return FRSVT_EINVAL;
-  h->use_tc = impl >= 1 ? 1 : 0;
-  h->pass2 = impl == 2 ? 1 : 0;
+  const int saved = h->use_tc;
+  h->use_tc = 0;
   frsvt_status st;
   if (h->esz == 4) {
     st = kind == 0 ? gemm_AX<float>(h, (const float*)A, lda, (const float*)B, (float*)out, nullptr)
@@ -1604,24 +1557,23 @@ static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t imp
                    : gemm_AtQ<double>(h, (const double*)A, lda, (const double*)B, (double*)out);
   }
   h->use_tc = saved;
-  h->pass2 = saved2;
   return st;
 }
 
 frsvt_status frsvt_debug_small_svd(frsvt_handle* h, int32_t impl, const double* G, double* Gcopy, double* sigma,
                                    double* UB, int32_t* sweeps, int32_t reps, double* ms) {
-  if (!h || !sigma || !UB || impl < 0 || impl > 2 || reps < 0) return FRSVT_EINVAL;
+  if (!h || !sigma || !UB || impl != 0 || reps < 0) return FRSVT_EINVAL;
   const size_t gb = sizeof(double) * h->l * h->l;
   if (G) CK(cudaMemcpyAsync(h->G, G, gb, cudaMemcpyDeviceToDevice, h->st));
   if (Gcopy) CK(cudaMemcpyAsync(Gcopy, h->G, gb, cudaMemcpyDeviceToDevice, h->st));
   CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
-  TRY(launch_eig(h, impl, h->G, sigma, UB));
+  TRY(launch_eig_jacobi(h, h->G, sigma, UB, 0, 0.0, nullptr));
   if (reps > 0) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, h->st));
-    for (int i = 0; i < reps; ++i) TRY(launch_eig(h, impl, h->G, sigma, UB));
+    for (int i = 0; i < reps; ++i) TRY(launch_eig_jacobi(h, h->G, sigma, UB, 0, 0.0, nullptr));
     CK(cudaEventRecord(e1, h->st));
     CK(cudaEventSynchronize(e1));
     float t = 0.f;
@@ -1683,8 +1635,6 @@ frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, v
   CK(cudaMemcpyAsync(h->G, G, sizeof(double) * h->l * h->l, cudaMemcpyDeviceToDevice, h->st));
   int* rd = h->lwd + 4;  // scratch int (lwd[0..3]: Loewdin flags)
   CK(cudaMemcpyAsync(rd, &r, sizeof(int), cudaMemcpyHostToDevice, h->st));
-  CK(cudaFuncSetAttribute(chol_inv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)chol_inv_smem_bytes()));
   chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, h->l, rd, 1e-12, (float*)T, h->l,
                                                                           &h->dev->s, &h->dev->flags, nullptr,
                                                                           stamps);

@@ -117,40 +117,3 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
 }
 
 }  // namespace frsvt
-
-namespace frsvt {
-// fp64 throughput probe (test hook only): every thread runs 8 independent
-// chains of `reps` DFMAs (kind 0) or every warp 8 independent DMMA chains
-// (kind 1); out[0] = cycles of CTA 0, out[1] = its flop count.
-__global__ void __launch_bounds__(512) fp64_rate_probe_kernel(int kind, int reps, float* __restrict__ out) {
-  double a[8], b[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    a[j] = 1.0 + 1e-9 * (threadIdx.x + j);
-    b[j] = 0.0;
-  }
-  __syncthreads();
-  const long long t0 = clock64();
-  if (kind == 0) {
-    for (int r = 0; r < reps; ++r) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = fma(a[j], 0.999999, b[j]);
-    }
-  } else {
-    for (int r = 0; r < reps; ++r) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_m8n8k4(b[2 * j], b[2 * j + 1], a[j], a[j + 4]);
-    }
-  }
-  __syncthreads();
-  const long long t1 = clock64();
-  double s = 0.0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) s += b[j];
-  if (s == 12345.0) out[2] = (float)s;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    out[0] = (float)(t1 - t0);
-    out[1] = kind == 0 ? (float)reps * 8.f * 2.f * blockDim.x : (float)reps * 4.f * 512.f * (blockDim.x / 32);
-  }
-}
-}  // namespace frsvt

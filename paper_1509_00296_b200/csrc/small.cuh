@@ -1,9 +1,5 @@
 // Small-matrix and elementwise kernels of libfrsvt (sm_100a).
 //   omega_kernel     : Gaussian test matrix Omega
-//   chol_piv_kernel  : pivoted, truncated Cholesky of an equilibrated fp64
-//                      Gram (CholeskyQR rank reveal, the QR-CP of P:163/P:177)
-//   jacobi_eig_kernel: cyclic two-sided Jacobi on the l x l fp64 Gram B B^T
-//                      -> U_B, sigma (the small SVD of B, Eq. 6)
 //   shrink_kernel    : thresholds t_i, d_i = max(sigma_i - t_i, 0), kept set,
 //                      the l x l factors of Eq. (6)
 //   reductions, ALM init, split-K reduce.
@@ -100,262 +96,6 @@ __global__ void __launch_bounds__(256) splitk_reduce_wide_kernel(const Tp* __res
   }
 }
 
-// ---- pivoted truncated Cholesky (single CTA, fp64, matrix in shared mem) ---
-// Input : G (l x l fp64 Gram, column-major, ld l).
-// Output: T (l x l, ld l) with Y*T = orth(Y) restricted to the revealed rank s:
-//         T[piv_k, j] = dsc[piv_k] * Rinv[k][j] for k <= j < s, 0 elsewhere,
-//         where diag(dsc) G diag(dsc) (unit diagonal) = Pi R^T R Pi^T.
-// A column whose equilibrated Schur diagonal falls to <= tol is numerically
-// dependent and truncates the factorisation (s = #pivots accepted).
-template <typename Tout>
-__global__ void __launch_bounds__(512)
-chol_piv_kernel(const double* __restrict__ G, int l, double tol, Tout* __restrict__ T,
-                int* __restrict__ s_out, int* __restrict__ flags) {
-  extern __shared__ double sm[];
-  double* S = sm;              // l*l, row-major
-  double* dsc = S + l * l;     // l
-  double* xt = dsc + l;        // l
-  double* dinv = xt + l;       // l
-  int* piv = (int*)(dinv + l); // l
-  int* ipiv = piv + l;         // l
-  __shared__ int s_sh, js_sh;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-
-  for (int i = tid; i < l; i += nt) {
-    const double g = G[i + (int64_t)i * l];
-    if (!isfinite(g)) atomicOr(flags, FLAG_NONFINITE);
-    dsc[i] = (g > 0.0 && isfinite(g)) ? 1.0 / sqrt(g) : 0.0;
-    piv[i] = i;
-  }
-  if (tid == 0) s_sh = l;
-  __syncthreads();
-  for (int idx = tid; idx < l * l; idx += nt) {
-    const int i = idx / l, c = idx % l;
-    double v = G[i + (int64_t)c * l] * dsc[i] * dsc[c];
-    S[idx] = isfinite(v) ? v : 0.0;
-  }
-  __syncthreads();
-
-  for (int k = 0; k < l; ++k) {
-    if (warp == 0) {
-      double best = -1.0;
-      int bj = l;
-      for (int j = k + lane; j < l; j += 32) {
-        const double v = S[j * l + j];
-        if (v > best) { best = v; bj = j; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
-      }
-      if (lane == 0) {
-        js_sh = bj;
-        if (!(best > tol)) s_sh = k;
-      }
-    }
-    __syncthreads();
-    if (s_sh == k) break;
-    const int js = js_sh;
-    if (js != k) {
-      for (int i = tid; i < l; i += nt) {
-        const double a = S[i * l + k];
-        S[i * l + k] = S[i * l + js];
-        S[i * l + js] = a;
-      }
-      __syncthreads();
-      for (int c = tid; c < l; c += nt) {
-        const double a = S[k * l + c];
-        S[k * l + c] = S[js * l + c];
-        S[js * l + c] = a;
-      }
-      if (tid == 0) { const int p = piv[k]; piv[k] = piv[js]; piv[js] = p; }
-      __syncthreads();
-    }
-    const double rkk = sqrt(S[k * l + k]);
-    for (int c = k + 1 + tid; c < l; c += nt) S[k * l + c] /= rkk;
-    __syncthreads();
-    if (tid == 0) S[k * l + k] = rkk;
-    const int w = l - k - 1;
-    for (int idx = tid; idx < w * w; idx += nt) {
-      const int i = k + 1 + idx / w, c = k + 1 + idx % w;
-      S[i * l + c] -= S[k * l + i] * S[k * l + c];
-    }
-    __syncthreads();
-  }
-  const int s = s_sh;
-  // In-place inverse of the s x s upper triangle R (column sweep, dtrti2 order):
-  // Rinv[i][j] = -dinv[j] * (dinv[i] R[i][j] + sum_{i<k<j} Rinv[i][k] R[k][j]).
-  for (int j = tid; j < s; j += nt) dinv[j] = 1.0 / S[j * l + j];
-  __syncthreads();
-  for (int j = 1; j < s; ++j) {
-    for (int i = warp; i < j; i += nw) {
-      double acc = 0.0;
-      for (int kk = i + 1 + lane; kk < j; kk += 32) acc += S[i * l + kk] * S[kk * l + j];
-      acc = warp_sum(acc);
-      if (lane == 0) xt[i] = acc + dinv[i] * S[i * l + j];
-    }
-    __syncthreads();
-    for (int i = tid; i < j; i += nt) S[i * l + j] = -dinv[j] * xt[i];
-    __syncthreads();
-  }
-  for (int j = tid; j < s; j += nt) S[j * l + j] = dinv[j];
-  for (int k = tid; k < l; k += nt) ipiv[piv[k]] = k;
-  __syncthreads();
-  for (int idx = tid; idx < l * l; idx += nt) {
-    const int o = idx % l, j = idx / l;  // T[o + j*l]
-    const int k = ipiv[o];
-    double v = 0.0;
-    if (j < s && k <= j) v = dsc[o] * S[k * l + j];
-    T[idx] = (Tout)v;
-  }
-  if (tid == 0) *s_out = s;
-}
-
-// ---- cyclic two-sided Jacobi on the symmetric l x l fp64 Gram -------------
-// Packed upper storage of G, round-robin (circle) pair ordering so the l/2
-// rotations of a round are disjoint and applied in parallel as 2x2 blocks
-// J_a^T G_ab J_b; V accumulates V J. A pair rotates when
-// |g_pq| > max(1e-15 sqrt(g_pp g_qq), 4 eps g_max); a sweep with no rotation
-// ends the solve. Outputs sigma = sqrt(max(lambda, 0)) descending and the
-// matching columns of V (U_B, ld l) in fp64.
-__device__ __forceinline__ int pk_idx(int i, int j, int l) {
-  // packed upper index of (min, max)
-  const int a = i < j ? i : j, b = i < j ? j : i;
-  return a * l - (a * (a - 1)) / 2 + (b - a);
-}
-
-__global__ void __launch_bounds__(1024)
-jacobi_eig_kernel(const double* __restrict__ G, int l, int max_sweeps,
-                  double* __restrict__ sigma, double* __restrict__ UB,
-                  int* __restrict__ sweeps_out, int* __restrict__ flags) {
-  extern __shared__ double sm[];
-  const int np = l * (l + 1) / 2;
-  double* P = sm;                 // packed G
-  double* V = P + np;             // l*l column-major V[i + c*l]
-  double* cs = V + l * l;         // FRSVT_LMAX/2 * 2 (c, s) per pair
-  int* pp = (int*)(cs + FRSVT_LMAX);       // p of pair
-  int* qq = pp + FRSVT_LMAX / 2;           // q of pair
-  int* act = qq + FRSVT_LMAX / 2;          // active flag per pair
-  __shared__ double red[32];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int L2 = (l + 1) & ~1;  // even number of players (dummy = l if l odd)
-  const int h = L2 / 2;
-
-  double gmax_local = 0.0;
-  for (int idx = tid; idx < l * l; idx += nt) {
-    const int i = idx % l, c = idx / l;
-    const double g = G[idx];
-    if (i <= c) P[pk_idx(i, c, l)] = g;
-    V[idx] = (i == c) ? 1.0 : 0.0;
-    if (i == c) gmax_local = fmax(gmax_local, fabs(g));
-  }
-  const double gmax = block_max(gmax_local, red);
-  __shared__ double gmax_sh;
-  if (tid == 0) gmax_sh = gmax;
-  __syncthreads();
-  const double abs_thr = 4.0 * 2.220446049250313e-16 * gmax_sh;
-
-  int sweep = 0;
-  bool converged = false;
-  for (sweep = 0; sweep < max_sweeps; ++sweep) {
-    int rotated = 0;
-    for (int rnd = 0; rnd < L2 - 1; ++rnd) {
-      int a_loc = 0;
-      if (tid < h) {
-        // circle method: position 0 fixed, the others rotate by one per round
-        const int pos_a = tid, pos_b = L2 - 1 - tid;
-        int p = pos_a == 0 ? 0 : 1 + ((pos_a - 1 + rnd) % (L2 - 1));
-        int q = pos_b == 0 ? 0 : 1 + ((pos_b - 1 + rnd) % (L2 - 1));
-        if (p > q) { const int t = p; p = q; q = t; }
-        pp[tid] = p;
-        qq[tid] = q;
-        double c = 1.0, s = 0.0;
-        if (q < l) {
-          const double apq = P[pk_idx(p, q, l)];
-          const double app = P[pk_idx(p, p, l)];
-          const double aqq = P[pk_idx(q, q, l)];
-          const double thr = fmax(1e-15 * sqrt(fabs(app * aqq)), abs_thr);
-          if (fabs(apq) > thr) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-            a_loc = 1;
-          }
-        }
-        cs[2 * tid] = c;
-        cs[2 * tid + 1] = s;
-        act[tid] = a_loc;
-      }
-      if (!__syncthreads_or(a_loc)) continue;
-      rotated = 1;
-      // G <- J^T G J, block (a, b) with b <= a
-      const int nblk = h * (h + 1) / 2;
-      for (int idx = tid; idx < nblk; idx += nt) {
-        int a = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-        while ((a + 1) * (a + 2) / 2 <= idx) ++a;
-        while (a * (a + 1) / 2 > idx) --a;
-        const int b = idx - a * (a + 1) / 2;
-        if (!act[a] && !act[b]) continue;
-        const int pa = pp[a], qa = qq[a], pb = pp[b], qb = qq[b];
-        const double ca = cs[2 * a], sa = cs[2 * a + 1];
-        const double cb = cs[2 * b], sb = cs[2 * b + 1];
-        if (a == b) {
-          const double app = P[pk_idx(pa, pa, l)], aqq = P[pk_idx(qa, qa, l)], apq = P[pk_idx(pa, qa, l)];
-          // J^T [[app,apq],[apq,aqq]] J with J = [[c, s], [-s, c]] (GVL symSchur2)
-          const double c2 = ca * ca, s2 = sa * sa, csx = ca * sa;
-          P[pk_idx(pa, pa, l)] = c2 * app - 2.0 * csx * apq + s2 * aqq;
-          P[pk_idx(qa, qa, l)] = s2 * app + 2.0 * csx * apq + c2 * aqq;
-          P[pk_idx(pa, qa, l)] = 0.0;
-        } else {
-          // rows {pa, qa} x cols {pb, qb}; the dummy player (index l) is absent
-          const bool ra = qa < l, rb = qb < l;
-          const double m00 = P[pk_idx(pa, pb, l)];
-          const double m01 = rb ? P[pk_idx(pa, qb, l)] : 0.0;
-          const double m10 = ra ? P[pk_idx(qa, pb, l)] : 0.0;
-          const double m11 = (ra && rb) ? P[pk_idx(qa, qb, l)] : 0.0;
-          const double n00 = ca * m00 - sa * m10, n01 = ca * m01 - sa * m11;
-          const double n10 = sa * m00 + ca * m10, n11 = sa * m01 + ca * m11;
-          P[pk_idx(pa, pb, l)] = n00 * cb - n01 * sb;
-          if (rb) P[pk_idx(pa, qb, l)] = n00 * sb + n01 * cb;
-          if (ra) P[pk_idx(qa, pb, l)] = n10 * cb - n11 * sb;
-          if (ra && rb) P[pk_idx(qa, qb, l)] = n10 * sb + n11 * cb;
-        }
-      }
-      // V <- V J  (columns p_b, q_b of every row)
-      for (int idx = tid; idx < l * h; idx += nt) {
-        const int i = idx % l, b = idx / l;
-        if (!act[b]) continue;
-        const int pb = pp[b], qb = qq[b];
-        const double cb = cs[2 * b], sb = cs[2 * b + 1];
-        const double vp = V[i + pb * l], vq = V[i + qb * l];
-        V[i + pb * l] = cb * vp - sb * vq;
-        V[i + qb * l] = sb * vp + cb * vq;
-      }
-      __syncthreads();
-    }
-    if (!rotated) { converged = true; break; }
-  }
-  __syncthreads();
-  // sort eigenvalues descending (rank by counting; ties by index)
-  for (int i = tid; i < l; i += nt) {
-    const double li = P[pk_idx(i, i, l)];
-    int rank = 0;
-    for (int j = 0; j < l; ++j) {
-      const double lj = P[pk_idx(j, j, l)];
-      rank += (lj > li) || (lj == li && j < i);
-    }
-    sigma[rank] = sqrt(fmax(li, 0.0));
-    for (int r = 0; r < l; ++r) UB[r + (int64_t)rank * l] = V[r + i * l];
-  }
-  if (tid == 0) {
-    *sweeps_out = converged ? sweep + 1 : sweep;
-    if (!converged) atomicOr(flags, FLAG_NOCONV);
-  }
-}
 
 // ---- shrinkage and the l x l factors of Eq. (6) ----------------------------
 // wmode: 0 tau (scalar: tau_dev ? *tau_dev : tau), 1 explicit w (device, l),

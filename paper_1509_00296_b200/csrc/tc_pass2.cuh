@@ -29,8 +29,7 @@
 // writes it directly; a tile split between CTAs leaves partial sums in a
 // per-CTA slot (first or last segment of the range), and the CTA that
 // finishes a split tile last (per-tile arrival counter) adds all its slots in
-// CTA order (deterministic; tc_fixup_kernel does it after the pass when the
-// counters are disabled). Small K (the l x l applies): whole tiles per CTA.
+// CTA order (deterministic). Small K (the l x l applies): whole tiles per CTA.
 //
 // Roles per CTA (640 threads; 2-CTA clusters multicast the B stages):
 //   warp 0      TMA producer of A (16 KB chunks, 4-deep ring, released as soon as
@@ -213,7 +212,7 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   // tile_cnt (nullable, >= mtiles zeros): in-kernel stream-K fixup. The CTA
   // that completes the last partial segment of a split tile sums all its
   // partial slots in CTA order (deterministic), writes the tile and re-arms
-  // the counter; without it tc_fixup_kernel does this afterwards.
+  // the counter (tile_cnt is required whenever a tile can be split).
   // rp_dev (MODE_AX, range propagation): r = *rp_dev carried columns; only the
   // p = Nvalid - r fresh columns are multiplied (B holds them at [0, p), the
   // MMA runs with N = roundup16(p)) and land in out[:, r + c]; out[:, :r] is a
@@ -607,67 +606,6 @@ tc_pass2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   if (threadIdx.x == 0) p2_cta_stamp(dbg, out, 3);
 }
 
-// Tiles split between CTAs: out = sum of the covering CTAs' partial slots (in
-// CTA order) (+ add). One block per tile; the covering CTAs and their slots
-// are resolved once per block (gridDim of the pass G <= 256).
-template <int NP, int CL>
-__global__ void __launch_bounds__(256) tc_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
-                                                       const float* __restrict__ part, float* __restrict__ out,
-                                                       int64_t ldo, const float* __restrict__ add, int64_t ldadd,
-                                                       const int* __restrict__ rp_dev) {
-  __shared__ int64_t soff[256];
-  __shared__ int ncov;
-  // G = number of work groups (clusters for CL = 2); group c's CTA for row
-  // tile t is c * CL + t % CL, its slots [cta][first|last segment]
-  const int nch = (Ktot + BK - 1) / BK;
-  const int mtiles = (Mtot + 127) / 128;
-  const int mgroups = (mtiles + CL - 1) / CL;
-  const int64_t total = (int64_t)mgroups * nch;
-  const int tile = blockIdx.x;
-  const int wt = tile / CL, crank = tile % CL;
-  const int cgrp = blockIdx.y, ngrp = gridDim.y;  // column groups of the tile
-  if (threadIdx.x == 0) {
-    const int64_t t0 = (int64_t)wt * nch, t1 = t0 + nch;
-    // CTAs whose range intersects [t0, t1)
-    int c0 = (int)((t0 * G) / total);
-    while (c0 > 0 && p2_range_begin(total, G, c0) > t0) --c0;
-    while (p2_range_begin(total, G, c0 + 1) <= t0) ++c0;
-    int c1 = c0;
-    while (c1 + 1 < G && p2_range_begin(total, G, c1 + 1) < t1) ++c1;
-    const bool whole = (c0 == c1) && p2_range_begin(total, G, c0) <= t0 && p2_range_begin(total, G, c0 + 1) >= t1;
-    int k = 0;
-    if (!whole) {
-      for (int cc = c0; cc <= c1 && k < 256; ++cc) {
-        const int64_t b = p2_range_begin(total, G, cc);
-        if (p2_range_begin(total, G, cc + 1) <= b) continue;  // empty range
-        const int slot = (b >= t0) ? 0 : 1;                      // tile holds the range's first / last segment
-        soff[k++] = ((int64_t)(cc * CL + crank) * P2_SLOTS + slot) * 128 * NP;
-      }
-    }
-    ncov = k;
-  }
-  __syncthreads();
-  const int nc = ncov;
-  if (nc == 0) return;  // written directly by the pass
-  const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
-  const int cpg = (Nvalid + ngrp - 1) / ngrp;
-  const int cb = cgrp * cpg, ce = min(Nvalid, cb + cpg);
-  for (int idx = threadIdx.x; idx < 128 * (ce - cb); idx += blockDim.x) {
-    const int row = idx & 127, c = cb + (idx >> 7);
-    const int gm = tile * 128 + row;
-    if (gm >= Mtot) continue;
-    if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
-      if (add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
-      continue;
-    }
-    const int ca = c - rsh;  // accumulator column
-    float acc = 0.f;
-    for (int k = 0; k < nc; ++k) acc += part[soff[k] + (int64_t)ca * 128 + row];
-    if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
-    out[gm + (int64_t)c * ldo] = acc;
-  }
-}
-
 // B operand split: Bh = rna_tf32(x) (fp32, rows x cols, ld ldh) and Bx (bf16,
 // (2 * roundup32(rows)) x cols, ld ldx): for K chunk c, Bx rows 64c + j hold
 // bf16(x - Bh) at K = 32c + j (j < 32) and bf16(Bh) at K = 32c + j - 32
@@ -706,122 +644,5 @@ __global__ void __launch_bounds__(256) split_tf32_bf16x2_kernel(const float* __r
   *reinterpret_cast<__nv_bfloat162*>(Bx + base + 32) = __floats2bfloat162_rn(h0, h1);
 }
 
-}  // namespace tc
-}  // namespace frsvt
-
-namespace frsvt {
-namespace tc {
-// Bandwidth probe (test hook only): streams the A operand of a pass through
-// the same persistent stream-K partition and TMA ring as tc_pass2_kernel, with
-// no math (one consumer warp releases each stage as soon as it lands).
-// Separates the DRAM/TMA streaming rate from the MMA/converter pipeline.
-template <int MODE, int SUB>
-__global__ void __launch_bounds__(64, 1)
-tma_stream_probe_kernel(const __grid_constant__ CUtensorMap mapA, int Mtot, int Ktot, float* __restrict__ sink) {
-  constexpr int ST = 8 / SUB;
-  constexpr uint32_t SUB_BYTES = 128u * BK * 4u;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + ST * SUB * SUB_BYTES);
-  uint64_t* empty = full + ST;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nch = (Ktot + BK * SUB - 1) / (BK * SUB);
-  const int mtiles = (Mtot + 127) / 128;
-  const int64_t total = (int64_t)mtiles * nch;
-  const int64_t g0 = p2_range_begin(total, gridDim.x, blockIdx.x), g1 = p2_range_begin(total, gridDim.x, blockIdx.x + 1);
-  const int nloc = (int)(g1 - g0);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < nloc; ++i) {
-      const int64_t g = g0 + i;
-      const int tile = (int)(g / nch), kc = (int)(g - (int64_t)tile * nch) * BK * SUB;
-      const int s = i % ST;
-      mbar_wait(&empty[s], ((i / ST) & 1) ^ 1);
-      mbar_expect_tx(&full[s], SUB * SUB_BYTES);
-      for (int u = 0; u < SUB; ++u) {
-        uint8_t* dst = smem + (s * SUB + u) * SUB_BYTES;
-        if (MODE == MODE_AX)
-          tma_load_2d(dst, &mapA, &full[s], tile * 128, kc + u * BK);
-        else
-          tma_load_2d(dst, &mapA, &full[s], kc + u * BK, tile * 128);
-      }
-    }
-  } else if (warp == 1) {
-    float acc = 0.f;
-    for (int i = 0; i < nloc; ++i) {
-      const int s = i % ST;
-      mbar_wait(&full[s], (i / ST) & 1);
-      acc += ((const float*)(smem + s * SUB * SUB_BYTES))[lane];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    if (acc == 1234.5f) sink[blockIdx.x] = acc;
-  }
-}
-}  // namespace tc
-}  // namespace frsvt
-
-namespace frsvt {
-namespace tc {
-// Tensor-pipe rate probe (test hook only): one CTA per SM issues `reps`
-// groups of MMAs back to back into one TMEM accumulator (M = 128, N = 128),
-// A from TMEM, B from (uninitialised) shared memory; writes cycles per MMA of
-// CTA 0 to out[0]. kind 0: tf32 (K = 8), 1: bf16 (K = 16), 2: tf32 with the
-// A operand from shared memory (SS), 3: tf32 N = 256, 4: tf32 N = 120.
-__global__ void __launch_bounds__(128, 1) mma_rate_probe_kernel(int kind, int reps, float* __restrict__ out) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tslot;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) {
-    tmem_alloc(&tslot, 512);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tb = tslot;
-  if (warp == 1) {
-    const bool leader = elect_one();
-    const uint32_t sb = smem_u32(smem);
-    const uint64_t bd = desc_kmajor_sw128(sb), ad = desc_kmajor_sw128(sb + 32768);
-    const uint32_t it = idesc_tf32(128, kind == 3 ? 256 : (kind == 4 ? 120 : 128)), ib = idesc_bf16(128, 128);
-    long long t0 = clock64();
-    if (leader) {
-      for (int r = 0; r < reps; ++r) {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ko = (uint64_t)(kk * 32) >> 4;
-          if (kind == 0 || kind >= 3) mma_tf32_ts(tb, tb + 256 + kk * 8, bd + ko, it, 1u);
-          else if (kind == 1) mma_bf16_ts(tb, tb + 256 + kk * 8, bd + ko, ib, 1u);
-          else mma_tf32_ss(tb, ad + ko, bd + ko, it, 1u);
-        }
-      }
-      tc_commit(&bar);
-    }
-    __syncwarp();
-    mbar_wait(&bar, 0);
-    long long t1 = clock64();
-    if (leader && blockIdx.x == 0) out[0] = (float)(t1 - t0) / (float)(reps * 4);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tb, 512);
-  }
-}
 }  // namespace tc
 }  // namespace frsvt

@@ -38,7 +38,7 @@ def _gram(l, kind, seed):
     return 0.5 * (G + G.T), s
 
 
-@pytest.mark.parametrize("impl", [0, 2])
+@pytest.mark.parametrize("impl", [0])
 @pytest.mark.parametrize("l", [10, 37, 64, 120, 128])
 @pytest.mark.parametrize("kind", ["cluster", "graded", "deficient", "random"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])

@@ -21,23 +21,25 @@ def P():
 @pytest.mark.parametrize("kind", [0, 1])
 def test_tc_pass_matches_fp64(P, m, n, l, kind):
     g = torch.Generator(device="cuda").manual_seed(m + n + l + kind)
-    A = torch.randn((n, m), device="cuda", generator=g).t()          # column-major m x n
+    ldm = (m + 3) // 4 * 4  # TMA needs 16-byte column strides: ld padded to a multiple of 4
+    A = torch.randn((n, ldm), device="cuda", generator=g)[:, :m].t()  # column-major m x n, ld ldm
     A[::7] *= 1e3                                                       # wide dynamic range
     B = torch.randn(((n if kind == 0 else m), l), device="cuda", generator=g).t().contiguous().t()
     h = P.Frsvt(m, n, l, 1, dtype=torch.float32, seed=1)
     ref = (A.double() @ B.double()) if kind == 0 else (A.double().t() @ B.double())
-    out_tc = h.debug_pass(kind, 1, A, B)
     out_p2 = h.debug_pass(kind, 2, A, B)
     out_si = h.debug_pass(kind, 0, A, B)
     den = torch.linalg.norm(ref)
-    e_tc = float(torch.linalg.norm(out_tc.double() - ref) / den)
     e_p2 = float(torch.linalg.norm(out_p2.double() - ref) / den)
     e_si = float(torch.linalg.norm(out_si.double() - ref) / den)
     # fp32-level products: all within a few fp32 ulps of the fp64 product
     assert e_si < 1e-5, e_si  # SIMT accumulates K in fp32 (long K: ~5e-6)
-    assert e_tc < 1e-5, e_tc
     assert e_p2 < 1e-5, e_p2
+    # element-wise: every output within fp32-level error of its |A||B| bound
+    # (a wrong tail element cannot hide in the Frobenius ratio)
+    bound = (A.double().abs() @ B.double().abs()) if kind == 0 else (A.double().abs().t() @ B.double().abs())
+    assert float(((out_p2.double() - ref).abs() / bound.clamp_min(1e-300)).max()) < 2e-5
     # a plain 1xTF32 product would be ~1e-4 off: the split really is in effect
-    assert max(e_tc, e_p2) < 0.1 * 2.0 ** -11
+    assert e_p2 < 0.1 * 2.0 ** -11
     # the stream-K pass is deterministic
     assert torch.equal(out_p2, h.debug_pass(kind, 2, A, B))
