@@ -53,6 +53,11 @@ typedef enum {
 
 typedef enum { FRSVT_F32 = 0, FRSVT_F64 = 1 } frsvt_dtype;
 
+#define FRSVT_LOOPBACK_MAX 8  /* ranks of a loopback group */
+
+/* Loopback process group (see frsvt_loopback_create). */
+typedef struct frsvt_group frsvt_group;
+
 /* info.flags bits */
 #define FRSVT_FLAG_NONFINITE 1
 #define FRSVT_FLAG_NOCONV 2
@@ -72,6 +77,7 @@ typedef struct {
   int32_t rank;             /* 0 .. nranks-1 */
   const unsigned char* nccl_id; /* host, 128 bytes from frsvt_get_unique_id on rank 0; NULL if nranks == 1 */
   uint32_t options;         /* FRSVT_OPT_* bits (0 = defaults) */
+  frsvt_group* group;       /* nranks > 1 without NCCL: the loopback group all ranks share (nccl_id ignored); NULL otherwise */
 } frsvt_config;
 
 /* frsvt_config.options bits */
@@ -91,6 +97,19 @@ typedef struct {
 } frsvt_info;
 
 typedef struct frsvt_handle frsvt_handle;
+
+/* Loopback process group of `nranks` (2..FRSVT_LOOPBACK_MAX) virtual ranks:
+ * the row-sharded path on ONE device and in ONE process,
+ * each rank a handle created with cfg.group = this group, driven by its own
+ * host thread and CUDA stream. Every all-reduce point of the path becomes a
+ * host rendezvous: the last rank to arrive enqueues one kernel that sums (or
+ * takes max/min over) all ranks' buffers in rank order and writes the result
+ * into each of them; every rank's stream is ordered after it with events. No
+ * kernel waits on another kernel. Collective calls (create, apply, step)
+ * must be issued by all ranks in the same order. Not CUDA-graph capturable.
+ * The caller destroys the group after every handle that uses it. */
+frsvt_status frsvt_loopback_create(int32_t nranks, frsvt_group** out);
+void frsvt_loopback_destroy(frsvt_group* g);
 
 /* 128-byte NCCL unique id (rank 0 only); the caller broadcasts it, e.g. with
  * torch.distributed, and passes it to frsvt_create on every rank. */
@@ -189,15 +208,17 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h);
 /* Test hook: one streaming pass on a chosen route (synchronises).
  * kind 0: out (m_local x l, ld m_local) = A (m_local x n) * B (n x l, ld n)
  * kind 1: out (n x l, ld n) = A^T * B (m_local x l, ld m_local), summed over ranks
- * impl 0 = SIMT CUDA cores, 2 = the persistent stream-K tcgen05 pass of the
- * product path (fp32 handles; needs lda % 4 == 0 and a 16-byte aligned A,
- * else FRSVT_EINVAL). */
+ * impl 0 = SIMT CUDA cores; 2 = the CTA-pair stream-K tcgen05 pass of the
+ * product path, exact (fp32-level products); 3 = the same pass with the
+ * tf32-rounded B, i.e. out = A * rna_tf32(B) (the span-only passes, DESIGN
+ * reading R17). 2 and 3 need an fp32 handle, lda % 4 == 0 and a 16-byte
+ * aligned A, else FRSVT_EINVAL. */
 frsvt_status frsvt_debug_pass(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                               const void* B, void* out);
 /* Same pass `reps` times back to back on the handle's stream (no host sync
  * in between), *ms = mean device time per pass (CUDA events). impl as above,
- * plus 8..135: the stream-K pass with parts of its pipeline switched off
- * (bit field impl - 8, see tc_pass2.cuh; outputs not meaningful). Synchronises. */
+ * plus 8..263: impl 2 with parts of its pipeline switched off (bit field
+ * impl - 8, see tc_pass3.cuh; outputs not meaningful). Synchronises. */
 frsvt_status frsvt_debug_pass_timed(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                                     const void* B, void* out, int32_t reps, double* ms);
 

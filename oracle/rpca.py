@@ -51,13 +51,24 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
     Y = D / max(norm2, np.max(np.abs(D)) / lam)
     L = np.zeros_like(D)
     E = np.zeros_like(D)
+    T = np.empty_like(D)     # scratch: D - L + Y/mu, then D - L - E
+    Ymu = np.empty_like(D)   # Y / mu
     carry = None
     hist = dict(r=[], s=[], resid=[], nrmse=[], mu=[])
     states = []
     nD = np.linalg.norm(D)
+    nL0 = None if L0 is None else np.linalg.norm(L0)
+    # The updates are written in place (BASELINE c5 is 65536 x 8192: every
+    # m x n temporary is 4.3 GB in fp64); each expression keeps the textbook
+    # evaluation order, so the values are those of the plain expressions
+    # E = S(D - L + Y/mu), A = D - E + Y/mu, Y = Y + mu (D - L - E).
     for k in range(n_iter):
-        E = soft_shrink(D - L + Y / mu, lam / mu)
-        Aop = D - E + Y / mu
+        np.divide(Y, mu, out=Ymu)
+        np.subtract(D, L, out=T)
+        T += Ymu
+        soft_shrink_into(T, lam / mu, E)
+        Aop = np.subtract(D, E, out=T)
+        Aop += Ymu
         if backend == "exact":
             L, _, r = svt_exact(Aop, 1.0 / mu)
             s = min(m, n)
@@ -70,17 +81,38 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
                                    Omega=np.array(Om, dtype=np.float64)))
             res = frsvt(Aop, Om, l, q, tau=1.0 / mu, carry=carry, rp=rp)
             L, r, s, new_carry = res.X, res.r, res.s, res.carry
+            del res
         carry = new_carry if rp else None
-        Y = Y + mu * (D - L - E)
+        np.subtract(D, L, out=T)
+        T -= E
         hist["r"].append(r)
         hist["s"].append(s)
-        hist["resid"].append(np.linalg.norm(D - L - E) / nD)
+        hist["resid"].append(np.linalg.norm(T) / nD)
         hist["mu"].append(mu)
+        T *= mu
+        Y += T
         if L0 is not None:
-            hist["nrmse"].append(np.linalg.norm(L - L0) / np.linalg.norm(L0))
+            hist["nrmse"].append(_fro_diff(L, L0) / nL0)
         mu = min(rho * mu, mu_bar)
     return dict(L=L, E=E, Y=Y, mu=mu, mu0=mu0, lam=lam, norm2=norm2, hist=hist,
                 states=states, carry=carry)
+
+
+def soft_shrink_into(x, tau, out):
+    """out = S_tau(x) = sgn(x) max(|x| - tau, 0), without temporaries."""
+    np.abs(x, out=out)
+    out -= tau
+    np.maximum(out, 0.0, out=out)
+    np.copysign(out, x, out=out)
+    return out
+
+
+def _fro_diff(X, Y, block=1024):
+    """||X - Y||_F over column blocks (no m x n temporary)."""
+    acc = 0.0
+    for j in range(0, X.shape[1], block):
+        acc += float(np.sum((X[:, j:j + block] - Y[:, j:j + block]) ** 2))
+    return float(np.sqrt(acc))
 
 
 def reweighted_wsvt(A, n_calls, l, q, C, eps, omega_fn, rp=True):

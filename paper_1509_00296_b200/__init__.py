@@ -16,7 +16,7 @@ import torch
 from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, FrsvtConfig, FrsvtInfo,
                    RpcaState, load_library, status_string)
 
-__all__ = ["Frsvt", "FrsvtError", "lib", "library_path", "colmajor", "W_EXPLICIT",
+__all__ = ["Frsvt", "FrsvtError", "LoopbackGroup", "lib", "library_path", "colmajor", "W_EXPLICIT",
            "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH"]
 
 W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
@@ -54,12 +54,37 @@ def _ld(x, rows, dtype, name):
     return x.stride(1)
 
 
+class LoopbackGroup:
+    """frsvt_loopback_create: `nranks` virtual ranks of the row-sharded path on
+    one device, one handle (Frsvt(..., group=g)) and host thread per rank."""
+
+    def __init__(self, nranks):
+        self._g = ctypes.c_void_p()
+        self.nranks = int(nranks)
+        _check("frsvt_loopback_create", lib.frsvt_loopback_create(self.nranks, ctypes.byref(self._g)))
+
+    @property
+    def ptr(self):
+        return self._g
+
+    def close(self):
+        if self._g.value:
+            lib.frsvt_loopback_destroy(self._g)
+            self._g = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Frsvt:
     """One FRSVT handle: fixed shape (m_local x n), sketch width l, power
     iterations q, range propagation flag, dtype (torch.float32/float64)."""
 
     def __init__(self, m, n, l, q=1, rp=True, dtype=torch.float32, seed=0, stream=None,
-                 nranks=1, rank=0, m_global=None, row0=0, nccl_id=None, device=None, options=0):
+                 nranks=1, rank=0, m_global=None, row0=0, nccl_id=None, device=None, options=0, group=None):
         if device is not None:
             torch.cuda.set_device(device)
         self.m, self.n, self.l, self.q, self.rp = int(m), int(n), int(l), int(q), bool(rp)
@@ -78,6 +103,9 @@ class Frsvt:
         cfg.nranks = int(nranks)
         cfg.rank = int(rank)
         cfg.options = int(options)
+        self._group = group
+        if group is not None:
+            cfg.group = group.ptr.value
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = (ctypes.c_ubyte * 128)(*bytes(nccl_id))

@@ -10,7 +10,7 @@ LIB_PATH = os.path.join(_HERE, "libfrsvt.so")
 
 # every entry point include/frsvt.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
-    "frsvt_get_unique_id", "frsvt_create", "frsvt_destroy", "frsvt_status_string",
+    "frsvt_loopback_create", "frsvt_loopback_destroy", "frsvt_get_unique_id", "frsvt_create", "frsvt_destroy", "frsvt_status_string",
     "frsvt_apply", "frsvt_apply_weighted", "rpca_alm_step", "frsvt_set_omega",
     "frsvt_draw_omega", "frsvt_get_carry", "frsvt_set_carry", "frsvt_reset_carry",
     "frsvt_set_call_index", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
@@ -24,7 +24,8 @@ class FrsvtConfig(ctypes.Structure):
                 ("m_global", ctypes.c_int64), ("row0", ctypes.c_int64), ("l", ctypes.c_int32),
                 ("q", ctypes.c_int32), ("range_propagation", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("nccl_id", ctypes.POINTER(ctypes.c_ubyte)), ("options", ctypes.c_uint32)]
+                ("nccl_id", ctypes.POINTER(ctypes.c_ubyte)), ("options", ctypes.c_uint32),
+                ("group", ctypes.c_void_p)]
 
 FRSVT_OPT_FUSED_SKETCH = 1
 
@@ -51,6 +52,8 @@ def load_library(path=LIB_PATH):
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     P = ctypes.POINTER
     sig = {
+        "frsvt_loopback_create": (i32, [i32, P(vp)]),
+        "frsvt_loopback_destroy": (None, [vp]),
         "frsvt_get_unique_id": (i32, [P(ctypes.c_ubyte)]),
         "frsvt_create": (i32, [P(FrsvtConfig), vp, P(vp)]),
         "frsvt_destroy": (None, [vp]),

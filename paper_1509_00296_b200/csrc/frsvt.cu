@@ -24,7 +24,7 @@
 #include "gram_dmma.cuh"
 #include "tc_pass.cuh"
 #include "tc_compose.cuh"
-#include "tc_pass2.cuh"
+#include "tc_util.cuh"
 #include "tc_compose2.cuh"
 #include "tc_pass3.cuh"
 
@@ -32,9 +32,11 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -56,7 +58,45 @@ struct Status {
   frsvt_status st = FRSVT_OK;
 };
 
+// Loopback reduction: out_r[i] = op over ranks k = 0..n-1 (in that order) of
+// in_k[i], written back into every rank's buffer (in place: each element is
+// read from all ranks before it is written).
+struct LoopPtrs {
+  void* p[FRSVT_LOOPBACK_MAX];
+};
+template <typename T>
+__global__ void loopback_reduce_kernel(LoopPtrs b, int n, size_t count, int op) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    T acc = reinterpret_cast<T*>(b.p[0])[i];
+    for (int k = 1; k < n; ++k) {
+      const T x = reinterpret_cast<T*>(b.p[k])[i];
+      acc = op == 0 ? acc + x : (op == 1 ? (x > acc ? x : acc) : (x < acc ? x : acc));
+    }
+    for (int k = 0; k < n; ++k) reinterpret_cast<T*>(b.p[k])[i] = acc;
+  }
+}
+
 }  // namespace
+
+// Loopback process group (include/frsvt.h): n handles of one process on one
+// device, each on its own host thread and stream. A reduction point is a host
+// rendezvous: every rank records an event on its stream; the last to arrive
+// makes its stream wait for all of them and enqueues one reduction kernel over
+// all ranks' buffers; every rank's stream then waits for that kernel. No
+// kernel waits on another kernel (stream-order dependencies only).
+struct frsvt_group {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  void* bufs[FRSVT_LOOPBACK_MAX] = {};
+  cudaEvent_t ready[FRSVT_LOOPBACK_MAX] = {};
+  cudaEvent_t done = nullptr;
+  size_t count = 0;
+  int type = 0, op = 0;
+  bool mismatch = false;
+};
 
 struct frsvt_handle {
   frsvt_config cfg;
@@ -106,6 +146,8 @@ struct frsvt_handle {
   int64_t call;
   int override_pending;
   ncclComm_t comm;
+  frsvt_group* group;    // loopback process group (nranks > 1 without NCCL), not owned
+  cudaEvent_t ev_ready;  // this rank's arrival at a loopback reduction
   int64_t launches;
   double last_mu_host;
   // pass profiling (frsvt_profile)
@@ -344,83 +386,6 @@ __global__ void sketch_width_kernel(const int* __restrict__ r_dev, int l, int th
   }
 }
 
-// ---- persistent stream-K passes (tc_pass2.cuh) ------------------------------
-// stream-K passes run on 2-CTA clusters (the B stages multicast to the pair)
-constexpr int P2_CL = 2;
-
-template <int MODE, int NP>
-frsvt_status launch_p2_np(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBl,
-                          int Mtot, int Ktot, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg,
-                          const int* rp_dev, const int* skip_dev = nullptr) {
-  constexpr int CL = P2_CL;
-  const size_t smem = tc::Pass2Smem::total(NP, tc::p2_astages(NP));  // attribute set in frsvt_create
-  const int mtiles = (int)cdiv(Mtot, 128);
-  const int64_t mgroups = cdiv(mtiles, CL);
-  const int64_t total = mgroups * cdiv(Ktot, tc::BK);
-  const int Gmax = h->nsm / CL;
-  // small K (the l x l applies of the orthonormalisation): whole tiles per
-  // work group, no split tiles (dbg bit 8)
-  const bool talign = Ktot <= 8 * tc::BK && !(dbg & 96);
-  if (talign) dbg |= 256;
-  const int64_t units = talign ? mgroups : total;
-  const int G = (int)(units < Gmax ? units : Gmax);  // work groups (clusters)
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(G * CL));
-  lc.blockDim = dim3(tc::P2_THREADS);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = h->st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  if (mtiles > h->ncnt) return FRSVT_EINVAL;  // the tile counters cover every row tile (sized at create)
-  CK(cudaLaunchKernelEx(&lc, tc::tc_pass2_kernel<MODE, NP, CL>, mA, mBh, mBl, Mtot, Ktot, h->l, h->l, out, ldo, add,
-                        ldadd, h->skpart, rp_dev, dbg, h->tilecnt, skip_dev));
-  (void)G;
-  return post_launch(h);
-}
-
-// out (Mtot x l) = op(A) * B, B (Ktot x l, ld ldb) the small operand:
-// MODE_AX: A is Mtot x Ktot (lda); MODE_ATQ: A is Ktot x Mtot (lda), op = ^T.
-template <int MODE>
-frsvt_status tc_pass2(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot, int64_t Ktot, const float* B,
-                      int64_t ldb, float* out, int64_t ldo, const float* add, int64_t ldadd, int dbg = 0,
-                      const int* rp_dev = nullptr, const int* skip_dev = nullptr, int np_force = 0) {
-  // np_force: N tile of the instance (0: by l); a narrower instance multiplies
-  // only the first np_force columns of B (the RP sketch when p is small)
-  const int np = np_force ? np_force : tc_np(h->l);
-  float* Bh = MODE == tc::MODE_AX ? h->Xh : h->Qh;
-  __nv_bfloat16* Bl = MODE == tc::MODE_AX ? h->Xb : h->Qb;
-  const int64_t ldh = MODE == tc::MODE_AX ? h->ldxs : h->ldqs;
-  const int64_t kx = cdiv(Ktot, tc::BK) * 2 * tc::BK;  // rows of the bf16 [b_l | b_h] operand
-  tc::split_tf32_bf16x2_kernel<<<dim3((unsigned)cdiv(kx / 2, 512), (unsigned)h->l), 256, 0, h->st>>>(
-      B, Ktot, h->l, ldb, Bh, ldh, Bl, h->ldb16);
-  TRY(post_launch(h));
-  CUtensorMap mA, mBh, mBl;
-  const uint32_t nb = (uint32_t)np / 2;  // each CTA of the pair loads an np/2-row half of a B stage
-  bool ok = (MODE == tc::MODE_AX) ? make_map(&mA, A, Mtot, Ktot, lda, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE)
-                                  : make_map(&mA, A, Ktot, Mtot, lda, tc::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok = ok && make_map(&mBh, Bh, Ktot, h->l, ldh, tc::BK, nb, CU_TENSOR_MAP_SWIZZLE_128B);
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)kx, (cuuint64_t)h->l};
-    cuuint64_t strides[1] = {(cuuint64_t)h->ldb16 * 2};
-    cuuint32_t box[2] = {(cuuint32_t)(2 * tc::BK), nb};
-    cuuint32_t es[2] = {1, 1};
-    ok = ok && g_encode(&mBl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)Bl, dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  }
-  if (!ok) return FRSVT_ECUDA;
-  if (np == 32)
-    return launch_p2_np<MODE, 32>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
-  if (np == 64)
-    return launch_p2_np<MODE, 64>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
-  return launch_p2_np<MODE, 128>(h, mA, mBh, mBl, (int)Mtot, (int)Ktot, out, ldo, add, ldadd, dbg, rp_dev, skip_dev);
-}
-
 // ---- CTA-pair (cta_group::2) stream-K passes (tc_pass3.cuh) -----------------
 template <int MODE, int NP, int TERMS>
 frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap& mBh, const CUtensorMap& mBx,
@@ -617,8 +582,51 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   return post_launch(h);
 }
 
+frsvt_status loopback_allreduce(frsvt_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
+  frsvt_group* g = h->group;
+  const int type = t == ncclFloat64 ? 0 : (t == ncclFloat32 ? 1 : 2);
+  const int o = op == ncclSum ? 0 : (op == ncclMax ? 1 : 2);
+  if ((t != ncclFloat64 && t != ncclFloat32 && t != ncclInt32) || (op != ncclSum && op != ncclMax && op != ncclMin))
+    return FRSVT_EINVAL;
+  std::unique_lock<std::mutex> lk(g->mu);
+  const int me = h->cfg.rank;
+  if (cudaEventRecord(h->ev_ready, h->st) != cudaSuccess) return FRSVT_ECUDA;
+  g->bufs[me] = buf;
+  g->ready[me] = h->ev_ready;
+  if (g->arrived == 0) {
+    g->count = count;
+    g->type = type;
+    g->op = o;
+  } else if (g->count != count || g->type != type || g->op != o) {
+    g->mismatch = true;  // ranks disagree on the reduction sequence
+  }
+  const uint64_t my_gen = g->gen;
+  if (++g->arrived == g->n) {
+    for (int r = 0; r < g->n; ++r)
+      if (r != me) CK(cudaStreamWaitEvent(h->st, g->ready[r], 0));
+    LoopPtrs ptrs{};
+    for (int r = 0; r < g->n; ++r) ptrs.p[r] = g->bufs[r];
+    const int blocks = (int)((count + 255) / 256 < 1024 ? (count + 255) / 256 : 1024);
+    if (type == 0) loopback_reduce_kernel<double><<<blocks, 256, 0, h->st>>>(ptrs, g->n, count, o);
+    else if (type == 1) loopback_reduce_kernel<float><<<blocks, 256, 0, h->st>>>(ptrs, g->n, count, o);
+    else loopback_reduce_kernel<int><<<blocks, 256, 0, h->st>>>(ptrs, g->n, count, o);
+    TRY(post_launch(h));
+    CK(cudaEventRecord(g->done, h->st));
+    g->arrived = 0;
+    g->gen++;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->gen != my_gen; });
+  }
+  // inside the lock: the next reduction cannot re-record `done` before every
+  // rank has ordered its stream after this one
+  CK(cudaStreamWaitEvent(h->st, g->done, 0));
+  return g->mismatch ? FRSVT_EINVAL : FRSVT_OK;
+}
+
 frsvt_status allreduce(frsvt_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op) {
   if (h->cfg.nranks <= 1) return FRSVT_OK;
+  if (h->group) return loopback_allreduce(h, buf, count, t, op);
   CKN(ncclAllReduce(buf, buf, count, t, op, h->comm, h->st));
   return FRSVT_OK;
 }
@@ -690,8 +698,8 @@ template <typename T>
 frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, bool m_rows, const T* Msm, T* Out) {
   if constexpr (sizeof(T) == 4) {
     if (tc_small_ok(h, rows, m_rows))  // stream-K pass with K = l: whole tiles per CTA pair
-      return tc_pass2<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows,
-                                   nullptr, 0);
+      return tc_pass3<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows,
+                                   nullptr, 0, 3);
   }
   return apply_small<T>(h, In, rows, rows, Msm, Out, rows);
 }
@@ -743,12 +751,12 @@ frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Ou
     int* flags = h->lwd + 8;
     sketch_width_kernel<<<1, 32, 0, h->st>>>(r_dev, l, 32, flags);
     TRY(post_launch(h));
-    TRY(tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev,
+    TRY(tc_pass3<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 3, 0, r_dev,
                               flags + 1));
-    return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev,
+    return tc_pass3<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 3, 0, r_dev,
                                  flags, 32);
   }
-  return tc_pass2<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 0, r_dev);
+  return tc_pass3<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 3, 0, r_dev);
 }
 
 // CholeskyQR, first pass (readings R2/R4/R14 in DESIGN.md): fp64 Gram,
@@ -780,14 +788,15 @@ frsvt_status orth_final(frsvt_handle* h, const T* In, int64_t rows, T* Out, bool
   return FRSVT_OK;
 }
 
-// Y (m x l) = A (m x n) * X (n x l)  [+ Add]
+// Y (m x l) = A (m x n) * X (n x l)  [+ Add]. terms (tensor path): 3 exact,
+// 2 with the tf32-rounded X (span-only passes, reading R17)
 template <typename T>
-frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y, const T* Add) {
+frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y, const T* Add, int terms) {
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
-      TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)X, h->n, (float*)Y, h->m,
-                                (const float*)Add, h->m));
+      TRY(tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)X, h->n, (float*)Y, h->m,
+                                (const float*)Add, h->m, terms));
       return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
     }
   }
@@ -802,14 +811,15 @@ frsvt_status gemm_AX(frsvt_handle* h, const T* A, int64_t lda, const T* X, T* Y,
   return prof_end(h, 0, (double)h->m * h->n * sizeof(T));
 }
 
-// Z (n x l) = A^T (n x m) * Q (m x l), split-K over rows, all-reduced over ranks
+// Z (n x l) = A^T (n x m) * Q (m x l), split-K over rows, all-reduced over
+// ranks. terms as in gemm_AX (3 for B^T = A^T Q, which enters X directly)
 template <typename T>
-frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z) {
+frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z, int terms) {
   if constexpr (sizeof(T) == 4) {
     if (tc_eligible(h, A, lda)) {
       TRY(prof_begin(h));
-      TRY(tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)Q, h->m, (float*)Z, h->n,
-                                 nullptr, 0));
+      TRY(tc_pass3<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)Q, h->m, (float*)Z, h->n,
+                                 nullptr, 0, terms));
       TRY(prof_end(h, 1, (double)h->m * h->n * sizeof(T)));
       TRY(allreduce(h, Z, (size_t)h->n * h->l, nccl_type<T>(), ncclSum));
       return FRSVT_OK;
@@ -856,19 +866,19 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
         sketch_width_kernel<<<1, 32, 0, h->st>>>(&h->dev->r, h->l, 32, flags);
         TRY(post_launch(h));
         CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
-        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
-                                  h->m, nullptr, 0, 0, &h->dev->r, flags + 1));
-        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
-                                  h->m, nullptr, 0, 0, &h->dev->r, flags, 32));
+        TRY(tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, nullptr, 0, 2, 0, &h->dev->r, flags + 1));
+        TRY(tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, nullptr, 0, 2, 0, &h->dev->r, flags, 32));
       } else {
-        TRY(tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
-                                  h->m, (const float*)h->Qt, h->m, 0, &h->dev->r, skip));
+        TRY(tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
+                                  h->m, (const float*)h->Qt, h->m, 2, 0, &h->dev->r, skip));
       }
       if (!skip) TRY(prof_end(h, 0, (double)h->m * h->n * sizeof(T)));
     }
   }
   h->fs_armed = false;
-  if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr));
+  if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr, 2));
   h->t2_pending = 0;
   if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true);
   // with range propagation on the tensor path the sketch basis is formed in
@@ -883,9 +893,9 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
     TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
   }
   for (int it = 0; it < q; ++it) {
-    TRY(gemm_AtQ<T>(h, A, lda, it == 0 ? Qcur : (const T*)h->Q, (T*)h->Z));
+    TRY(gemm_AtQ<T>(h, A, lda, it == 0 ? Qcur : (const T*)h->Q, (T*)h->Z, 2));
     TRY(orth1<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, false));
-    TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr));
+    TRY(gemm_AX<T>(h, A, lda, (const T*)h->Zq, (T*)h->Y, nullptr, 2));
     if (it + 1 < q) TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
     else TRY(orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
   }
@@ -913,7 +923,7 @@ frsvt_status launch_eig_jacobi(frsvt_handle* h, const double* G, double* sigma, 
 template <typename T>
 frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0, double t_host = 0.0,
                        const double* t_dev = nullptr) {
-  TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z));
+  TRY(gemm_AtQ<T>(h, A, lda, (const T*)h->Q, (T*)h->Z, 3));
   TRY(gram<T>(h, (const T*)h->Z, h->n, h->n, false));
   if (h->t2_pending) {  // G = T2^T (Z'^T Z') T2 for B^T = Z' T2
     TRY(gemm_ll<double>(h, h->G, 0, h->T2d, 0, h->Hd));
@@ -1144,12 +1154,6 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 32>), tc::PassSmem::total(32));
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 64>), tc::PassSmem::total(64));
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 128>), tc::PassSmem::total(128));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 32, P2_CL>), tc::Pass2Smem::total(32, tc::p2_astages(32)));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 64, P2_CL>), tc::Pass2Smem::total(64, tc::p2_astages(64)));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_AX, 128, P2_CL>), tc::Pass2Smem::total(128, tc::p2_astages(128)));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 32, P2_CL>), tc::Pass2Smem::total(32, tc::p2_astages(32)));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 64, P2_CL>), tc::Pass2Smem::total(64, tc::p2_astages(64)));
-  FRSVT_ATTR((tc::tc_pass2_kernel<tc::MODE_ATQ, 128, P2_CL>), tc::Pass2Smem::total(128, tc::p2_astages(128)));
 #define FRSVT_ATTR3(MODE, NPV, TV) FRSVT_ATTR((tc::tc_pass3_kernel<MODE, NPV, TV>), tc::Pass3Smem::total(NPV, TV))
   FRSVT_ATTR3(tc::MODE_AX, 32, 2);
   FRSVT_ATTR3(tc::MODE_AX, 64, 2);
@@ -1200,6 +1204,28 @@ const char* frsvt_status_string(frsvt_status s) {
   return "unknown status";
 }
 
+frsvt_status frsvt_loopback_create(int32_t nranks, frsvt_group** out) {
+  if (!out) return FRSVT_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || nranks > FRSVT_LOOPBACK_MAX) return FRSVT_EINVAL;
+  frsvt_group* g = new (std::nothrow) frsvt_group();
+  if (!g) return FRSVT_ENOMEM;
+  g->n = nranks;
+  if (cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    delete g;
+    return FRSVT_ECUDA;
+  }
+  *out = g;
+  return FRSVT_OK;
+}
+
+void frsvt_loopback_destroy(frsvt_group* g) {
+  if (!g) return;
+  if (g->done) cudaEventDestroy(g->done);
+  delete g;
+}
+
 frsvt_status frsvt_get_unique_id(unsigned char out[128]) {
   if (!out) return FRSVT_EINVAL;
   ncclUniqueId id;
@@ -1217,6 +1243,7 @@ static void free_handle(frsvt_handle* h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->comm) ncclCommDestroy(h->comm);
+  if (h->ev_ready) cudaEventDestroy(h->ev_ready);
   if (h->prof_ev) {
     for (cudaEvent_t e : *h->prof_ev) cudaEventDestroy(e);
     delete h->prof_ev;
@@ -1237,7 +1264,8 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   if (c.q < 0 || c.q > 64) return FRSVT_EINVAL;
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks) return FRSVT_EINVAL;
   if (c.nranks == 1 && c.m_local != c.m_global) return FRSVT_EINVAL;
-  if (c.nranks > 1 && !c.nccl_id) return FRSVT_EINVAL;
+  if (c.nranks > 1 && !c.nccl_id && !c.group) return FRSVT_EINVAL;
+  if (c.group && (c.group->n != c.nranks || c.nranks > FRSVT_LOOPBACK_MAX)) return FRSVT_EINVAL;
   if (c.m_local > (int64_t)INT32_MAX || c.n > (int64_t)INT32_MAX) return FRSVT_EINVAL;
 
   frsvt_handle* h = new (std::nothrow) frsvt_handle();
@@ -1340,7 +1368,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
       return FRSVT_ENOMEM;
     }
     if (c.dtype == FRSVT_F32 &&
-        (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P2_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
+        (cudaMalloc((void**)&h->skpart, (size_t)nsm * tc::P3_SLOTS * 128 * 128 * sizeof(float)) != cudaSuccess ||
          cudaMalloc((void**)&h->Xb, (size_t)h->ldb16 * l * 2) != cudaSuccess ||
          cudaMalloc((void**)&h->Qb, (size_t)h->ldb16 * l * 2) != cudaSuccess)) {
       cudaGetLastError();
@@ -1358,17 +1386,26 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
     return FRSVT_ECUDA;
   }
   if (c.nranks > 1) {
-    ncclUniqueId id;
-    memcpy(&id, c.nccl_id, 128);
-    if (ncclCommInitRank(&h->comm, c.nranks, id, c.rank) != ncclSuccess) {
-      free_handle(h);
-      return FRSVT_ENCCL;
+    if (c.group) {
+      h->group = c.group;
+      if (cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        free_handle(h);
+        return FRSVT_ECUDA;
+      }
+    } else {
+      ncclUniqueId id;
+      memcpy(&id, c.nccl_id, 128);
+      if (ncclCommInitRank(&h->comm, c.nranks, id, c.rank) != ncclSuccess) {
+        free_handle(h);
+        return FRSVT_ENCCL;
+      }
     }
     // rank-uniform path choices (the tensor-core orthonormalisation of the
     // m-row matrices depends on m_local): agree on the minimum over ranks
     int* flag = h->lwd + 6;
     if (cudaMemcpyAsync(flag, &h->tc_m, sizeof(int), cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
-        ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, h->comm, h->st) != ncclSuccess ||
+        allreduce(h, flag, 1, ncclInt32, ncclMin) != FRSVT_OK ||
         cudaMemcpyAsync(&h->tc_m, flag, sizeof(int), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
         cudaStreamSynchronize(h->st) != cudaSuccess) {
       cudaGetLastError();
@@ -1525,36 +1562,31 @@ int64_t frsvt_kernel_launches(const frsvt_handle* h) { return h ? h->launches : 
 
 static frsvt_status debug_pass_nosync(frsvt_handle* h, int32_t kind, int32_t impl, const void* A, int64_t lda,
                                       const void* B, void* out) {
-  // impl 0: SIMT passes; 2: the stream-K tcgen05 pass; 8..135: the same pass
-  // with parts of its pipeline disabled (dbg = impl - 8, outputs invalid)
+  // impl 0: SIMT passes; 2: the CTA-pair tcgen05 pass of the product path
+  // (exact, 3 terms); 3: the same with the tf32-rounded small operand (2
+  // terms, the span-only passes); 8..263: impl 2 with parts of its pipeline
+  // switched off (dbg = impl - 8, outputs invalid)
   if (!h || !A || !B || !out || lda < h->m || kind < 0 || kind > 1 || impl < 0 || impl > 263 || impl == 1 ||
-      (impl >= 5 && impl < 8))
+      (impl >= 4 && impl < 8))
     return FRSVT_EINVAL;
   if (impl >= 2 && !(h->esz == 4 && h->use_tc && tc_eligible(h, A, lda))) return FRSVT_EINVAL;
-  if (impl == 3 || impl == 4 || impl >= 136) {  // CTA-pair pass: 3 exact, 4 tf32-rounded B, 136.. probes
-    const int terms = impl == 4 ? 2 : 3;
-    const int dbg = impl >= 136 ? impl - 136 : 0;
+  if (impl >= 2) {
+    const int terms = impl == 3 ? 2 : 3;
+    const int dbg = impl >= 8 ? impl - 8 : 0;
     return kind == 0 ? tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n, (float*)out,
                                              h->m, nullptr, 0, terms, dbg)
                      : tc_pass3<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m,
                                               (float*)out, h->n, nullptr, 0, terms, dbg);
   }
-  if (impl >= 2) {
-    const int dbg = impl >= 8 ? impl - 8 : 0;
-    return kind == 0 ? tc_pass2<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)B, h->n, (float*)out,
-                                             h->m, nullptr, 0, dbg)
-                     : tc_pass2<tc::MODE_ATQ>(h, (const float*)A, lda, h->n, h->m, (const float*)B, h->m, (float*)out,
-                                              h->n, nullptr, 0, dbg);
-  }
   const int saved = h->use_tc;
   h->use_tc = 0;
   frsvt_status st;
   if (h->esz == 4) {
-    st = kind == 0 ? gemm_AX<float>(h, (const float*)A, lda, (const float*)B, (float*)out, nullptr)
-                   : gemm_AtQ<float>(h, (const float*)A, lda, (const float*)B, (float*)out);
+    st = kind == 0 ? gemm_AX<float>(h, (const float*)A, lda, (const float*)B, (float*)out, nullptr, 3)
+                   : gemm_AtQ<float>(h, (const float*)A, lda, (const float*)B, (float*)out, 3);
   } else {
-    st = kind == 0 ? gemm_AX<double>(h, (const double*)A, lda, (const double*)B, (double*)out, nullptr)
-                   : gemm_AtQ<double>(h, (const double*)A, lda, (const double*)B, (double*)out);
+    st = kind == 0 ? gemm_AX<double>(h, (const double*)A, lda, (const double*)B, (double*)out, nullptr, 3)
+                   : gemm_AtQ<double>(h, (const double*)A, lda, (const double*)B, (double*)out, 3);
   }
   h->use_tc = saved;
   return st;

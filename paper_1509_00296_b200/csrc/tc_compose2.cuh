@@ -24,7 +24,7 @@
 //              direct stores of E', A' (or L)
 #pragma once
 #include "tc_compose.cuh"
-#include "tc_pass2.cuh"
+#include "tc_util.cuh"
 
 namespace frsvt {
 namespace tc {

@@ -45,20 +45,49 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
-#include "tc_pass2.cuh"
+#include "tc_util.cuh"
 
 namespace frsvt {
 namespace tc {
 
 constexpr int P3_THREADS = 640;
 constexpr int P3_SLOTS = 2;  // partial-tile slots per CTA
-constexpr int P3_SEG = 8;    // chunks accumulated in TMEM before a flush
+#ifndef P3_SEG_CH
+#define P3_SEG_CH 8
+#endif
+#ifndef P3_BST_WIDE
+#define P3_BST_WIDE 6
+#endif
+#ifndef P3_AST_WIDE
+#define P3_AST_WIDE 6
+#endif
+constexpr int P3_SEG = P3_SEG_CH;  // chunks accumulated in TMEM before a flush
 
 // A ring (16 KB stages) and B ring depth of an instance
 __host__ __device__ constexpr int p3_astages(int np, int terms) {
-  return np <= 32 ? 8 : (terms == 2 ? 7 : 6);
+  return np <= 32 ? 8 : (terms == 2 ? P3_AST_WIDE + 1 : P3_AST_WIDE);
 }
-__host__ __device__ constexpr int p3_bstages(int np, int terms) { return np <= 32 ? 8 : 6; }
+__host__ __device__ constexpr int p3_bstages(int np, int terms) { return np <= 32 ? 8 : P3_BST_WIDE; }
+
+// the chunk range of a cluster as accumulator pieces of <= P3_SEG chunks,
+// never crossing a tile (all roles iterate it identically)
+struct P3Walk {
+  int64_t g, g1;  // next chunk, end of range
+  int nch;        // chunks per tile
+  __device__ __forceinline__ bool next(int& tile, int& k0, int& k1, bool& tile_first, bool& tile_last,
+                                       int64_t& seg_begin) {
+    if (g >= g1) return false;
+    tile = (int)(g / nch);
+    k0 = (int)(g - (int64_t)tile * nch);
+    const int64_t end = min(g1, (int64_t)(tile + 1) * nch);
+    tile_first = (g == seg_begin);
+    k1 = (int)min((int64_t)(k0 + P3_SEG), end - (int64_t)tile * nch);
+    g = (int64_t)tile * nch + k1;
+    tile_last = (g == end);
+    if (tile_last) seg_begin = g;
+    return true;
+  }
+};
 // TMEM A ring: stage stride in columns, number of stages (accumulators use 0..255)
 __host__ __device__ constexpr int p3_tstride(int terms) { return terms == 3 ? 64 : 48; }
 __host__ __device__ constexpr int p3_tstages(int terms) { return terms == 3 ? 4 : 5; }
@@ -81,23 +110,16 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-// arrive on the barrier at the same offset in CTA `rank` of the cluster
+// arrive on the barrier at the same offset in CTA `rank` of the cluster. The
+// data handed over this way lives in TMEM (ordered by tcgen05.wait::st and
+// tcgen05.fence::before_thread_sync on the arriving side, fence::after on the
+// MMA side) or is a TMEM read that completed (tcgen05.wait::ld), so the
+// default CTA-scope release suffices; a .release.cluster arrive measured
+// ~0.7 us per arrival on B200 (a cluster-scope fence per call).
 __device__ __forceinline__ void mbar_arrive_rank(uint64_t* bar, uint32_t rank) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_u32(smem_u32(bar), rank))
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa_u32(smem_u32(bar), rank)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
-  const uint32_t a = smem_u32(b);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, "
-        "p;\n}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) { mbar_wait(b, parity); }
 // TMA 2D load into this CTA's shared memory whose transaction bytes complete
 // on the barrier at cluster address `bar_cluster` (the leader CTA's)
 __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1,
@@ -149,7 +171,8 @@ __device__ __forceinline__ void arrive_pair(uint64_t* bar) {
 }
 
 // dbg (test hook only, 0 in production): bit 0 no MMA, bit 1 no conversion,
-// bit 2 no B loads, bit 8 whole work tiles per cluster (small K, set by the host)
+// bit 2 no B loads, bit 4 no accumulator reads (flush), bit 8 whole work
+// tiles per cluster (small K, set by the host)
 template <int MODE, int NP, int TERMS>
 __global__ void __launch_bounds__(P3_THREADS, 1)
 tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
@@ -201,8 +224,8 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const int64_t total = (int64_t)mgroups * nch;
   const int G = gridDim.x / CL, cta = blockIdx.x, cgrp = blockIdx.x / CL;
   const bool talign = (dbg & 256) != 0;
-  const int64_t g0 = talign ? ((int64_t)mgroups * cgrp / G) * nch : p2_range_begin(total, G, cgrp);
-  const int64_t g1 = talign ? ((int64_t)mgroups * (cgrp + 1) / G) * nch : p2_range_begin(total, G, cgrp + 1);
+  const int64_t g0 = talign ? ((int64_t)mgroups * cgrp / G) * nch : sk_range_begin(total, G, cgrp);
+  const int64_t g1 = talign ? ((int64_t)mgroups * (cgrp + 1) / G) * nch : sk_range_begin(total, G, cgrp + 1);
   const int nloc = (int)(g1 - g0);
 
   if (threadIdx.x == 0) {
@@ -282,7 +305,7 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const uint32_t id_tf = idesc_tf32(256, nmma);
       const uint32_t id_bf = idesc_bf16(256, nmma);
       const bool elected = elect_one();
-      P2Walk wk{g0, g1, nch};
+      P3Walk wk{g0, g1, nch};
       int64_t sb = g0;
       int tile, k0, k1;
       bool tf, tl;
@@ -412,7 +435,7 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     float sum[HALF];
 #pragma unroll
     for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
-    P2Walk wk{g0, g1, nch};
+    P3Walk wk{g0, g1, nch};
     int64_t sb = g0;
     int tile, k0, k1;
     bool tf, tl;
@@ -423,13 +446,15 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const int b = piece & 1;
       mbar_wait(&accfull[b], (piece >> 1) & 1);
       tc_fence_after();
+      if (!(dbg & 16)) {
 #pragma unroll
-      for (int cb = 0; cb < HALF; cb += 16) {
-        uint32_t v[16];
-        tmem_ld16(t_acc0 + 128 * b + col0 + cb + lane_off, v);
-        tc_wait_ld();
+        for (int cb = 0; cb < HALF; cb += 16) {
+          uint32_t v[16];
+          tmem_ld16(t_acc0 + 128 * b + col0 + cb + lane_off, v);
+          tc_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) sum[cb + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) sum[cb + j] += __uint_as_float(v[j]);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -470,12 +495,12 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           if (warp == 12 && lane == 0) {
             const int64_t t0 = (int64_t)tile * nch, t1 = t0 + nch;
             int c0 = (int)((t0 * G) / total);
-            while (c0 > 0 && p2_range_begin(total, G, c0) > t0) --c0;
-            while (p2_range_begin(total, G, c0 + 1) <= t0) ++c0;
+            while (c0 > 0 && sk_range_begin(total, G, c0) > t0) --c0;
+            while (sk_range_begin(total, G, c0 + 1) <= t0) ++c0;
             int c1 = c0;
-            while (c1 + 1 < G && p2_range_begin(total, G, c1 + 1) < t1) ++c1;
+            while (c1 + 1 < G && sk_range_begin(total, G, c1 + 1) < t1) ++c1;
             int nc = 0;
-            for (int cc = c0; cc <= c1; ++cc) nc += (p2_range_begin(total, G, cc + 1) > p2_range_begin(total, G, cc));
+            for (int cc = c0; cc <= c1; ++cc) nc += (sk_range_begin(total, G, cc + 1) > sk_range_begin(total, G, cc));
             const int atile = tile * CL + (int)crank;
             const unsigned int old = atomicAdd(&tile_cnt[atile], 1u);
             s_last = (old + 1 == (unsigned int)nc) ? 1 : 0;
@@ -491,8 +516,8 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
             for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
             for (int cc = s_c0; cc <= s_c1; ++cc) {
-              const int64_t bg = p2_range_begin(total, G, cc);
-              if (p2_range_begin(total, G, cc + 1) <= bg) continue;
+              const int64_t bg = sk_range_begin(total, G, cc);
+              if (sk_range_begin(total, G, cc + 1) <= bg) continue;
               const int sl = (bg >= t0) ? 0 : 1;
               const float* q = part + ((int64_t)(cc * CL + (int)crank) * P3_SLOTS + sl) * 128 * NP;
 #pragma unroll

@@ -43,3 +43,11 @@ def test_tc_pass_matches_fp64(P, m, n, l, kind):
     assert e_p2 < 0.1 * 2.0 ** -11
     # the stream-K pass is deterministic
     assert torch.equal(out_p2, h.debug_pass(kind, 2, A, B))
+    # span-only route (impl 3, reading R17): the product of the exact A with
+    # the tf32-rounded B, at the same fp32 level
+    Bt = (B.t().contiguous().view(torch.int32).add(0x1000).bitwise_and(~0x1FFF)).view(torch.float32).t()
+    ref_t = (A.double() @ Bt.double()) if kind == 0 else (A.double().t() @ Bt.double())
+    out_t = h.debug_pass(kind, 3, A, B)
+    assert float(torch.linalg.norm(out_t.double() - ref_t) / torch.linalg.norm(ref_t)) < 1e-5
+    bound_t = (A.double().abs() @ Bt.double().abs()) if kind == 0 else (A.double().abs().t() @ Bt.double().abs())
+    assert float(((out_t.double() - ref_t).abs() / bound_t.clamp_min(1e-300)).max()) < 2e-5
