@@ -31,12 +31,18 @@ from .svt import soft_shrink, svt_exact
 
 def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
               mu_max_factor=1e7, norm2=None, L0=None, backend="frsvt",
-              record_states=False):
+              record_states=False, ap=None, varsigma_alpha=None):
     """Returns dict with L, E, Y, mu and per-iteration history.
 
     omega_fn(k) -> Omega (n x l) for iteration k (call index k).
     record_states: keep (E_{k+1}, operand A_k, mu_k, carry_k, Omega_k) of
     every iteration for teacher-forced parity.
+    ap: adaptive rank prediction (oracle/adaptive.py), a dict with
+    a, rho_n (= ceil(rho n)), b (<= l) and optionally l0 (default ceil(0.1 b)):
+    call k sketches with width l_k (RP: p_k = l_k - r_{k-1} fresh columns, the
+    first ones of Omega), and l_{k+1} follows Eq. (7). hist["l"] records l_k.
+    varsigma_alpha: record hist["varsigma"], the Prop. 4 estimate of each
+    call's sketch.
     """
     D = np.asarray(D, dtype=np.float64)
     m, n = D.shape
@@ -54,7 +60,12 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
     T = np.empty_like(D)     # scratch: D - L + Y/mu, then D - L - E
     Ymu = np.empty_like(D)   # Y / mu
     carry = None
-    hist = dict(r=[], s=[], resid=[], nrmse=[], mu=[])
+    hist = dict(r=[], s=[], resid=[], nrmse=[], mu=[], l=[], varsigma=[])
+    l_cur = l
+    if ap is not None:
+        from .adaptive import ap_initial, ap_next
+        b_ap = min(int(ap["b"]), l)
+        l_cur = min(int(ap.get("l0", ap_initial(b_ap))), b_ap)
     states = []
     nD = np.linalg.norm(D)
     nL0 = None if L0 is None else np.linalg.norm(L0)
@@ -78,10 +89,19 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
             if record_states:
                 states.append(dict(E=E.copy(), A=Aop.copy(), mu=mu,
                                    carry=None if carry is None else carry.copy(),
-                                   Omega=np.array(Om, dtype=np.float64)))
-            res = frsvt(Aop, Om, l, q, tau=1.0 / mu, carry=carry, rp=rp)
+                                   Omega=np.array(Om, dtype=np.float64), l=l_cur))
+            if varsigma_alpha is not None:
+                from .adaptive import sketch_varsigma
+                r_c = 0 if carry is None else carry.shape[1]
+                nfresh = l_cur - r_c if (rp and r_c > 0) else l_cur
+                hist["varsigma"].append(sketch_varsigma(Aop, np.asarray(Om)[:, :max(nfresh, 1)],
+                                                        carry if (rp and r_c > 0) else None, varsigma_alpha))
+            res = frsvt(Aop, Om, l_cur, q, tau=1.0 / mu, carry=carry, rp=rp)
             L, r, s, new_carry = res.X, res.r, res.s, res.carry
             del res
+        hist["l"].append(l_cur)
+        if ap is not None:
+            _, l_cur = ap_next(r, l_cur, int(ap["a"]), int(ap["rho_n"]), b_ap)
         carry = new_carry if rp else None
         np.subtract(D, L, out=T)
         T -= E

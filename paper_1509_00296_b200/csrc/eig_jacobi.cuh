@@ -32,9 +32,18 @@
 //
 // A pair rotates when |g| > tol_rot sqrt(|m_p|^2 |m_q|^2), g = m_p . m_q.
 // The solve stops after a sweep with no rotation, or (tol_stop > 0) after a
-// sweep whose largest relative off-diagonal was <= tol_stop: Jacobi sweeps
-// converge quadratically, so the sweep that measured tol_stop leaves
-// off-diagonals near tol_stop^2 (fp32 handles: tol_stop 1e-4 -> ~1e-9 measured on c5).
+// sweep whose largest measured off-diagonal was <= tol_stop, measured as
+// g^2 / (|m_p|^2 |m_q|^2) (relative to both columns), except for a pair whose
+// smaller column is clearly below the scalar threshold t (sigma < t/2,
+// t_mode != 0): there g^2 / max(|m_p|^2, |m_q|^2)^2. With m = G v ~ lambda v,
+// an unresolved g perturbs the pair's eigenvectors by ~g / (lambda_p^2 -
+// lambda_q^2), which both measures bound, and over-estimates the smaller
+// eigenvalue by ~g^2 / lambda_p^2: relative to a kept eigenvalue that needs the
+// two-sided measure, while a clearly sub-threshold one stays below t. So a
+// kept column paired with a near-null one (fp32 rounding noise in B once the
+// revealed rank drops) no longer holds the solve open. Jacobi sweeps converge
+// quadratically: the sweep that measured tol_stop leaves off-diagonals near
+// tol_stop^2 (fp32 handles: tol_stop 1e-4).
 //
 // Exact shortcut (t_mode != 0): if the Gershgorin bound max_i sum_j |G_ij| is
 // <= t_min^2, every sigma_i <= t_min and every shrunk value
@@ -162,6 +171,10 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
   }
 
   const double tol2 = tol_rot * tol_rot;
+  // |m|^2 below which a column is clearly under the threshold (sigma < t/2,
+  // |G v|^2 = lambda^2 < t^4/16); 0 without a scalar threshold
+  const double tsmall = t2 > 0.0 ? t2 * t2 * (1.0 / 16.0) : 0.0;
+
   const int pj = lane >> 3;  // the pair this lane computes parameters for
   const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
   int sweep = 0;
@@ -250,7 +263,11 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
         double a = 0.0, b = 0.0;
         const bool rot = (cx < l) && (cy < l) && al > 0.0 && be > 0.0 && gg > tol2 * abv;
         if (rot) {
-          maxrel = fmax(maxrel, gg * eig_rcp_approx(abv));
+          // convergence measure (see the header): relative to the larger
+          // column when the smaller one is clearly below the threshold
+          const double mxn = fmax(al, be);
+          const double den = fmin(al, be) >= tsmall ? abv : mxn * mxn;
+          maxrel = fmax(maxrel, gg * eig_rcp_approx(den));
           // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
           // to ~1e-7 relative: any t defines an exact rotation once c, s are
           // consistent with it, an approximate angle only leaves a ~1e-7 fraction
