@@ -94,6 +94,12 @@ typedef struct {
   double sigma[FRSVT_LMAX]; /* singular values of B = Q^T A, descending (first s valid) */
   double d[FRSVT_LMAX];     /* shrunk values max(sigma_i - t_i, 0) */
   double mu;                /* rpca: mu used by the last step */
+  int32_t l_next;           /* sketch width of the next call (adaptive rank prediction; l otherwise) */
+  int32_t pad_;
+  double varsigma;          /* Prop. 4 estimate of the sketch's residual sigma:
+                               20 sqrt(2/pi) ||(I - QQ^T) y||, y the last fresh sample, Q the
+                               basis before it; >= sigma_{k+1}(A) with probability >= 95%.
+                               Reported by the tensor-core (fp32) path; 0 elsewhere. */
 } frsvt_info;
 
 typedef struct frsvt_handle frsvt_handle;
@@ -195,6 +201,16 @@ frsvt_status frsvt_draw_omega(frsvt_handle* h, int64_t call, void* out, int64_t 
 frsvt_status frsvt_get_carry(frsvt_handle* h, void* Qt, int64_t ldq, int32_t* r);
 frsvt_status frsvt_set_carry(frsvt_handle* h, const void* Qt, int64_t ldq, int32_t r);
 frsvt_status frsvt_reset_carry(frsvt_handle* h);
+/* Adaptive rank prediction (AP, §2.3, Eq. (7)): after a
+ * call with sketch width l_i and kept rank r_i, the next call uses
+ * l_{i+1} = min(r_i + p_{i+1}, b), p_{i+1} = a if r_i < l_i else p_jump
+ * (= ceil(rho n)); with range propagation it draws l_{i+1} - r_i fresh columns
+ * behind the r_i carried ones. Kept on the device (no host synchronisation;
+ * the handle's buffers stay sized for l: the inactive columns are zero and
+ * dropped by the rank reveal). l_0 = l0 after this call, after
+ * frsvt_reset_carry and at the init of every rpca solve. 1 <= b <= l,
+ * 1 <= l0 <= b, a, p_jump >= 1; a == 0 switches AP off. Synchronises. */
+frsvt_status frsvt_set_adaptive_rank(frsvt_handle* h, int32_t a, int32_t p_jump, int32_t b, int32_t l0);
 /* Set the Omega call counter (the next call draws Omega of call `call`). */
 frsvt_status frsvt_set_call_index(frsvt_handle* h, int64_t call);
 /* Last call's report (synchronises). */

@@ -226,6 +226,21 @@ class Frsvt:
     def reset_carry(self):
         _check("frsvt_reset_carry", lib.frsvt_reset_carry(self._h))
 
+    def set_adaptive_rank(self, a=2, p_jump=None, b=None, l0=None, rho=0.05, gamma=None):
+        """Adaptive rank prediction (Eq. 7): a, p_jump = ceil(rho n_min) (the
+        jump when the kept rank fills the sketch), bound b (default l, or
+        ceil(gamma n_min)), l0 (default ceil(0.1 b)). a=0 switches it off."""
+        import math
+        nmin = min(self.cfg.m_global, self.n)
+        if b is None:
+            b = self.l if gamma is None else min(self.l, int(math.ceil(gamma * nmin)))
+        if p_jump is None:
+            p_jump = max(1, int(math.ceil(rho * nmin)))
+        if l0 is None:
+            l0 = max(1, int(math.ceil(0.1 * b)))
+        _check("frsvt_set_adaptive_rank", lib.frsvt_set_adaptive_rank(self._h, int(a), int(p_jump), int(b), int(l0)))
+        return dict(a=a, rho_n=p_jump, b=b, l0=l0)
+
     def set_call_index(self, call):
         _check("frsvt_set_call_index", lib.frsvt_set_call_index(self._h, int(call)))
 

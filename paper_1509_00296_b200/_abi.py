@@ -13,7 +13,7 @@ SYMBOLS = [
     "frsvt_loopback_create", "frsvt_loopback_destroy", "frsvt_get_unique_id", "frsvt_create", "frsvt_destroy", "frsvt_status_string",
     "frsvt_apply", "frsvt_apply_weighted", "rpca_alm_step", "frsvt_set_omega",
     "frsvt_draw_omega", "frsvt_get_carry", "frsvt_set_carry", "frsvt_reset_carry",
-    "frsvt_set_call_index", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
+    "frsvt_set_call_index", "frsvt_set_adaptive_rank", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
     "frsvt_kernel_launches", "frsvt_profile", "frsvt_profile_read", "frsvt_debug_pass",
     "frsvt_debug_small_svd", "frsvt_debug_pass_timed", "frsvt_debug_chol", "frsvt_debug_chol_inv",
 ]
@@ -34,7 +34,8 @@ class FrsvtInfo(ctypes.Structure):
     _fields_ = [("s", ctypes.c_int32), ("r", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("sweeps", ctypes.c_int32), ("calls", ctypes.c_int64),
                 ("sigma", ctypes.c_double * FRSVT_LMAX), ("d", ctypes.c_double * FRSVT_LMAX),
-                ("mu", ctypes.c_double)]
+                ("mu", ctypes.c_double), ("l_next", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("varsigma", ctypes.c_double)]
 
 
 class RpcaState(ctypes.Structure):
@@ -67,6 +68,7 @@ def load_library(path=LIB_PATH):
         "frsvt_set_carry": (i32, [vp, vp, i64, i32]),
         "frsvt_reset_carry": (i32, [vp]),
         "frsvt_set_call_index": (i32, [vp, i64]),
+        "frsvt_set_adaptive_rank": (i32, [vp, i32, i32, i32, i32]),
         "frsvt_get_info": (i32, [vp, P(FrsvtInfo)]),
         "rpca_get_mu": (i32, [vp, P(dbl)]),
         "rpca_set_mu": (i32, [vp, dbl, dbl]),

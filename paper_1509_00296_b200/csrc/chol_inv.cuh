@@ -61,7 +61,10 @@ template <typename Tq>
 __global__ void __launch_bounds__(CI_THREADS, 1)
 chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_dev, double tol, Tq* __restrict__ T,
                 int64_t ldt, int* __restrict__ s_out, int* __restrict__ flags, const int* __restrict__ skip,
-                unsigned long long* __restrict__ prof = nullptr) {
+                unsigned long long* __restrict__ prof = nullptr, double* __restrict__ resid_last = nullptr) {
+  // resid_last (nullable): ||(I - Q Q^T) y||, y the last nonzero sample and Q
+  // a basis of the carry and the samples before it (the
+  // by-product behind the Prop. 4 estimate varsigma)
   if (skip && *skip) return;
   // prof (test hook, nullable): %globaltimer at phase boundaries
 #define CI_STAMP(q)                                          \
@@ -218,6 +221,15 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
     int s = r;
     for (int i = 0; i < p; ++i) s += (sd[i] > 0.0);
     *s_out = s;
+    if (resid_last) {
+      double res = 0.0;
+      for (int i = p - 1; i >= 0; --i)
+        if (dsc[i] > 0.0) {  // the last nonzero sample: its Schur diagonal, unequilibrated
+          res = sd[i] > 0.0 ? 1.0 / (sd[i] * dsc[i]) : 0.0;  // sqrt(d) / dsc (a dropped sample: ~0)
+          break;
+        }
+      *resid_last = res;
+    }
   }
 }
 

@@ -52,6 +52,8 @@ struct DevState {
   double dmax, dss;    // ||D||_inf, ||D||_F^2
   double resid[2];     // ||D-L-E||_F^2, relative residual
   double rep[2 * FRSVT_LMAX];
+  int p_ap, l_act;     // adaptive rank prediction: fresh columns and width of the next call
+  double varsig_raw;   // ||(I - QQ^T) y|| of the last sketch sample (Prop. 4 by-product)
 };
 
 struct Status {
@@ -118,6 +120,8 @@ struct frsvt_handle {
   int tc_m;          // tensor-core small-operand path for the m-row matrices (Y, Q); rank-uniform
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_OPT_FUSED_SKETCH)
+  int ap_on, ap_a, ap_jump, ap_b, ap_l0;  // adaptive rank prediction (Eq. 7), frsvt_set_adaptive_rank
+  double* resid_out;  // where the next sketch orthonormalisation reports its last-sample residual
   bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
   float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
   float* OmT;        // Omega^T, n x 24 (the fused sketch's TMA operand)
@@ -376,11 +380,34 @@ frsvt_status tc_AtQ_gen(frsvt_handle* h, const float* A, int64_t lda, int64_t ro
                                  (int64_t)Mcols * h->l, nullptr, 0);
 }
 
-// flags[0] = (p > thr), flags[1] = (p <= thr) for p = l - *r_dev (the skip
-// flags of the two sketch instances)
-__global__ void sketch_width_kernel(const int* __restrict__ r_dev, int l, int thr, int* __restrict__ flags) {
+// flags[0] = (p > thr), flags[1] = (p <= thr) for p = l - *r_dev, capped by
+// *pmax_dev when adaptive rank prediction is on (the skip flags of the two
+// sketch instances)
+// adaptive rank prediction, Eq. (7): from this call's
+// width l_i and kept rank r_i, p_{i+1} = a if r_i < l_i else ceil(rho n),
+// l_{i+1} = min(r_i + p_{i+1}, b); the next call draws l_{i+1} - r_i fresh
+// columns behind the r_i carried ones
+__global__ void ap_update_kernel(DevState* __restrict__ d, int a, int jump, int b) {
   if (threadIdx.x == 0) {
-    const int p = l - min(max(*r_dev, 0), l);
+    const int r = d->r, l = d->l_act;
+    const int p = r < l ? a : jump;
+    const int ln = min(r + p, b);
+    d->l_act = ln;
+    d->p_ap = ln - r;
+  }
+}
+__global__ void ap_reset_kernel(DevState* __restrict__ d, int l0) {
+  if (threadIdx.x == 0) {
+    d->l_act = l0;
+    d->p_ap = l0;
+  }
+}
+
+__global__ void sketch_width_kernel(const int* __restrict__ r_dev, int l, int thr, int* __restrict__ flags,
+                                    const int* __restrict__ pmax_dev) {
+  if (threadIdx.x == 0) {
+    int p = l - min(max(*r_dev, 0), l);
+    if (pmax_dev) p = min(p, max(*pmax_dev, 0));
     flags[0] = p > thr ? 1 : 0;
     flags[1] = p > thr ? 0 : 1;
   }
@@ -743,13 +770,15 @@ frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Ou
   const bool sharded = m_rows && h->cfg.nranks > 1;
   TRY(gram<float>(h, In, rows, rows, sharded, r_dev));
   chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, l, r_dev, 1e-12, (float*)h->T1, l,
-                                                                          &h->dev->s, &h->dev->flags, nullptr);
+                                                                          &h->dev->s, &h->dev->flags, nullptr,
+                                                                          nullptr, h->resid_out);
+  h->resid_out = nullptr;  // only the sketch's orthonormalisation reports it
   TRY(post_launch(h));
   // r_dev: in place (Out == In): only the fresh columns are written; with
   // p <= 32 on the 32-column instance (the device-side choice of R11)
   if (r_dev && l > 32) {
     int* flags = h->lwd + 8;
-    sketch_width_kernel<<<1, 32, 0, h->st>>>(r_dev, l, 32, flags);
+    sketch_width_kernel<<<1, 32, 0, h->st>>>(r_dev, l, 32, flags, h->ap_on ? &h->dev->p_ap : nullptr);
     TRY(post_launch(h));
     TRY(tc_pass3<tc::MODE_AX>(h, In, rows, rows, l, (const float*)h->T1, l, Out, rows, nullptr, 0, 3, 0, r_dev,
                               flags + 1));
@@ -839,7 +868,8 @@ frsvt_status gemm_AtQ(frsvt_handle* h, const T* A, int64_t lda, const T* Q, T* Z
 // range finder: Q (m x l) spanning (A A^T)^q A Omega' (+ Q~), Alg. 1 lines 3-15
 template <typename T>
 frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint32_t stream,
-                          bool use_carry, int64_t call) {
+                          bool use_carry, int64_t call, bool ap = true) {
+  const int* pmax = (ap && h->ap_on) ? &h->dev->p_ap : nullptr;  // adaptive rank prediction (Eq. 7)
   const int l = h->l;
   const T* ov = h->override_pending ? (const T*)h->OmOv : nullptr;
   // RP on the stream-K path: multiply only the p fresh columns (Alg. 1 RP
@@ -848,7 +878,11 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   if constexpr (sizeof(T) == 4) rp_front = use_carry && tc_eligible(h, A, lda);
   omega_kernel<T><<<grid1d(h->n * l), 256, 0, h->st>>>((T*)h->Om, h->n, l, &h->dev->r, use_carry ? 1 : 0,
                                                        h->cfg.seed, stream + (uint32_t)call, ov, h->n,
-                                                       rp_front ? 1 : 0);
+                                                       rp_front ? 1 : 0, pmax);
+  // the first orthonormalisation of the sketch reports the residual of its
+  // last sample (tensor path), the Prop. 4 by-product
+  CK(cudaMemsetAsync(&h->dev->varsig_raw, 0, sizeof(double), h->st));
+  h->resid_out = &h->dev->varsig_raw;
   TRY(post_launch(h));
   h->override_pending = 0;
   if constexpr (sizeof(T) == 4) {
@@ -863,7 +897,7 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
         // for this p (flags[0]: p > 32, flags[1]: p <= 32); the carried
         // columns are copied first (the narrow instance writes the fresh ones)
         int* flags = h->lwd + 8;
-        sketch_width_kernel<<<1, 32, 0, h->st>>>(&h->dev->r, h->l, 32, flags);
+        sketch_width_kernel<<<1, 32, 0, h->st>>>(&h->dev->r, h->l, 32, flags, pmax);
         TRY(post_launch(h));
         CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
         TRY(tc_pass3<tc::MODE_AX>(h, (const float*)A, lda, h->m, h->n, (const float*)h->Om, h->n, (float*)h->Y,
@@ -880,7 +914,11 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   h->fs_armed = false;
   if (!rp_front) TRY(gemm_AX<T>(h, A, lda, (const T*)h->Om, (T*)h->Y, use_carry ? (const T*)h->Qt : nullptr, 2));
   h->t2_pending = 0;
-  if (q == 0) return orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true);
+  if (q == 0) {
+    TRY(orth_final<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
+    h->resid_out = nullptr;
+    return FRSVT_OK;
+  }
   // with range propagation on the tensor path the sketch basis is formed in
   // place in Y: [Q~ | orth(Y_p - Q~ Q~^T Y_p)] (reading R11)
   const T* Qcur = (const T*)h->Q;
@@ -892,6 +930,7 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   } else {
     TRY(orth1<T>(h, (const T*)h->Y, h->m, (T*)h->Q, true));
   }
+  h->resid_out = nullptr;
   for (int it = 0; it < q; ++it) {
     TRY(gemm_AtQ<T>(h, A, lda, it == 0 ? Qcur : (const T*)h->Q, (T*)h->Z, 2));
     TRY(orth1<T>(h, (const T*)h->Z, h->n, (T*)h->Zq, false));
@@ -991,6 +1030,10 @@ frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, dou
   else if (wmode == 1) TRY(small_svd<T>(h, A, lda, 1, tau));
   else TRY(small_svd<T>(h, A, lda));
   TRY(shrink_and_factors<T>(h, wmode, tau, tau_dev, C, eps));
+  if (h->ap_on) {
+    ap_update_kernel<<<1, 32, 0, h->st>>>(h->dev, h->ap_a, h->ap_jump, h->ap_b);
+    TRY(post_launch(h));
+  }
   h->call++;
   return FRSVT_OK;
 }
@@ -1025,6 +1068,8 @@ frsvt_status fill_info(frsvt_handle* h, frsvt_info* info) {
   info->sweeps = ds.sweeps;
   info->calls = h->call;
   info->mu = ds.mu[0];
+  info->l_next = h->ap_on ? ds.l_act : h->l;
+  info->varsigma = 20.0 * sqrt(2.0 / M_PI) * ds.varsig_raw;
   for (int i = 0; i < FRSVT_LMAX; ++i) {
     info->sigma[i] = i < h->l ? ds.rep[i] : 0.0;
     info->d[i] = i < h->l ? ds.rep[FRSVT_LMAX + i] : 0.0;
@@ -1057,7 +1102,7 @@ frsvt_status apply_impl(frsvt_handle* h, const void* A, int64_t lda, int wmode, 
 template <typename T>
 frsvt_status estimate_norm2(frsvt_handle* h, const T* D, int64_t ld) {
   CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
-  TRY(range_finder<T>(h, D, ld, FRSVT_NORM2_Q, 999u, false, 0));
+  TRY(range_finder<T>(h, D, ld, FRSVT_NORM2_Q, 999u, false, 0, false));
   TRY(small_svd<T>(h, D, ld));
   return FRSVT_OK;
 }
@@ -1088,6 +1133,10 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
     CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
     CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
     CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
+    if (h->ap_on) {
+      ap_reset_kernel<<<1, 32, 0, h->st>>>(h->dev, h->ap_l0);
+      TRY(post_launch(h));
+    }
     h->call = 0;
     h->fs_armed = false;
   }
@@ -1108,7 +1157,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
       if (fs_next) {
         omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 1,
                                                                     h->cfg.seed, 1000u + (uint32_t)h->call, nullptr,
-                                                                    h->n, 1);
+                                                                    h->n, 1, h->ap_on ? &h->dev->p_ap : nullptr);
         TRY(post_launch(h));
         CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
       }
@@ -1527,6 +1576,29 @@ frsvt_status frsvt_reset_carry(frsvt_handle* h) {
   CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
   CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
   CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
+  if (h->ap_on) {
+    ap_reset_kernel<<<1, 32, 0, h->st>>>(h->dev, h->ap_l0);
+    TRY(post_launch(h));
+  }
+  return FRSVT_OK;
+}
+
+frsvt_status frsvt_set_adaptive_rank(frsvt_handle* h, int32_t a, int32_t p_jump, int32_t b, int32_t l0) {
+  if (!h) return FRSVT_EINVAL;
+  if (a == 0) {
+    h->ap_on = 0;
+    return FRSVT_OK;
+  }
+  if (a < 1 || p_jump < 1 || b < 1 || b > h->l || l0 < 1 || l0 > b) return FRSVT_EINVAL;
+  h->fs_armed = false;
+  h->ap_on = 1;
+  h->ap_a = a;
+  h->ap_jump = p_jump;
+  h->ap_b = b;
+  h->ap_l0 = l0;
+  ap_reset_kernel<<<1, 32, 0, h->st>>>(h->dev, l0);
+  TRY(post_launch(h));
+  CK(cudaStreamSynchronize(h->st));
   return FRSVT_OK;
 }
 

@@ -37,19 +37,24 @@ __device__ __forceinline__ double philox_normal(uint64_t seed, uint32_t stream, 
 // call (p = l - r, RP reading Z6), columns < r are zero so that
 // A * Omega' + Q~ = [Q~ | A Omega_p]. r = 0 without a carry. With front != 0
 // the p fresh columns sit at [0, p) instead (the stream-K sketch multiplies
-// only them and writes them behind the carried columns).
+// only them and writes them behind the carried columns). pmax_dev (nullable,
+// adaptive rank prediction P:204-215): at most *pmax_dev fresh columns, the
+// rest zero (a zero sample is dropped by the rank reveal, so the basis has
+// r + p columns: the sketch width of Eq. (7)).
 template <typename T>
 __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __restrict__ r_dev,
                              int use_r, uint64_t seed, uint32_t stream,
-                             const T* __restrict__ override_om, int64_t ldo, int front = 0) {
+                             const T* __restrict__ override_om, int64_t ldo, int front = 0,
+                             const int* __restrict__ pmax_dev = nullptr) {
   const int r = use_r ? *r_dev : 0;
+  const int p = pmax_dev ? min(l - r, max(*pmax_dev, 0)) : l - r;
   const int64_t total = n * (int64_t)l;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % n;
     const int c = (int)(idx / n);
     T v = T(0);
-    if (front ? (c < l - r) : (c >= r)) {
+    if (front ? (c < p) : (c >= r && c < r + p)) {
       const int src = front ? c : c - r;
       if (override_om) v = override_om[i + src * ldo];
       else v = (T)philox_normal(seed, stream, (uint64_t)src * (uint64_t)n + (uint64_t)i);
