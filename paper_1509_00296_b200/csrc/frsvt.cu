@@ -521,8 +521,9 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
                         int64_t ld, double rho, double lambda, int* nparts, bool fs_next = false) {
   const int Kp = h->Kp;
   // compose2 (the iALM epilogue) splits Q~ itself while moving it to TMEM
-  const bool tma_ok = (ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0;
-  const bool use2 = epi != tc::EPI_STORE && tma_ok && (h->m % 4) == 0;
+  const bool tma_ok = epi == tc::EPI_STORE ? ((ldx % 4) == 0 && ((uintptr_t)X % 16) == 0)
+                                           : ((ld % 4) == 0 && (((uintptr_t)D | (uintptr_t)A | (uintptr_t)E) % 16) == 0);
+  const bool use2 = tma_ok && (h->m % 4) == 0;
   {
     if (!use2) {
       dim3 g1((unsigned)cdiv(h->m, 32), (unsigned)(Kp / 32));
@@ -560,6 +561,10 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
     CUtensorMap mD, mA, mE, mQ;
     if (!make_map(&mQ, (const float*)h->Qt, h->m, h->l, h->m, 128, tc::BK, CU_TENSOR_MAP_SWIZZLE_NONE))
       return FRSVT_ECUDA;
+    if (epi == tc::EPI_STORE) {  // no streamed operands: placeholder maps (never read)
+      D = A = E = X;
+      ld = ldx;
+    }
     if (!make_map(&mD, D, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mE, E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !make_map(&mA, epi == tc::EPI_ALM ? A : E, h->m, h->n, ld, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -582,7 +587,8 @@ frsvt_status tc_compose(frsvt_handle* h, int epi, float* X, int64_t ldx, const f
   } while (0)
     if (epi == tc::EPI_ALM && fs) FRSVT_LAUNCH_CMP2(tc::EPI_ALM, true);
     else if (epi == tc::EPI_ALM) FRSVT_LAUNCH_CMP2(tc::EPI_ALM, false);
-    else FRSVT_LAUNCH_CMP2(tc::EPI_FINAL, false);
+    else if (epi == tc::EPI_FINAL) FRSVT_LAUNCH_CMP2(tc::EPI_FINAL, false);
+    else FRSVT_LAUNCH_CMP2(tc::EPI_STORE, false);
 #undef FRSVT_LAUNCH_CMP2
     if (nparts) *nparts = (int)grid.x;
     TRY(post_launch(h));
@@ -1220,6 +1226,7 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_ALM, false>), tc::Compose2Smem::total());
   FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_ALM, true>), tc::Compose2Smem::total());
   FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_FINAL, false>), tc::Compose2Smem::total());
+  FRSVT_ATTR((tc::tc_compose2_kernel<tc::EPI_STORE, false>), tc::Compose2Smem::total());
   FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_STORE>, tc::ComposeSmem::total());
   FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_ALM>, tc::ComposeSmem::total());
   FRSVT_ATTR(tc::tc_compose_kernel<tc::EPI_FINAL>, tc::ComposeSmem::total());

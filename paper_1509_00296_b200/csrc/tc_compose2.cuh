@@ -81,9 +81,10 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
                    float* __restrict__ Aop, float* __restrict__ E, int64_t ld, const double* __restrict__ mu,
                    double rho, double lambda, double* __restrict__ part, float* __restrict__ fspart,
                    int* __restrict__ fs_done) {
-  static_assert(EPI == EPI_ALM || EPI == EPI_FINAL, "compose2 streams D/E(/A)");
+  // EPI_STORE: X = Q~ Wt^T only (the FRSVT call's composition, Eq. (6)); no
+  // streamed operands, the epilogue writes X from the accumulator
   constexpr uint32_t CB = Compose2Smem::chunk_bytes;
-  constexpr int NARR = EPI == EPI_ALM ? 3 : 2;  // D, E (, A)
+  constexpr int NARR = EPI == EPI_ALM ? 3 : (EPI == EPI_FINAL ? 2 : 0);  // D, E (, A)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* ring = smem;                                   // C2_RING x 3 slices; first Q~ staging
@@ -171,7 +172,7 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {
+    if (lane == 0 && NARR > 0) {
       prefetch_tmap(&mapD);
       prefetch_tmap(&mapE);
       if (EPI == EPI_ALM) prefetch_tmap(&mapA);
@@ -286,6 +287,15 @@ tc_compose2_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       } else {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) v[jj] = 0u;
+      }
+      if (EPI == EPI_STORE) {
+        if (row < m) {
+          const int c0 = (jt0 + tl) * 128 + 8 * cc;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (c0 + jj < n) __stcs(X + row + (int64_t)(c0 + jj) * ldx, __uint_as_float(v[jj]));
+        }
+        continue;
       }
       mbar_wait(&sfull[s], (i / C2_RING) & 1);
       const float* st = reinterpret_cast<const float*>(ring + (size_t)s * C2_STAGE);
