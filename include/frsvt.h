@@ -188,6 +188,11 @@ typedef struct {
   double norm2_D;    /* > 0 supplied ||D||_2; 0 -> estimated on device at iter 0 */
   double mu0;        /* > 0 supplied mu_0; 0 -> 1.25 / ||D||_2 */
   int32_t iter;      /* in/out: k; incremented by every non-finalize step */
+  int32_t keep;      /* >= 0: partial SVT, the first `keep` singular values are not thresholded
+                        (Type B truncated nuclear norm: argmin sum_{i>keep} sigma_i(L) + lambda ||S||_1);
+                        0 = the nuclear norm (standard RPCA) */
+  int32_t transfer;  /* 1: the init (iter == 0) keeps the handle's carried basis Q~ (range propagation
+                        handles): the basis transfer between semi-online windows; 0: fresh */
 } rpca_state;
 
 frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, double* rel_resid);

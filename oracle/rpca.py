@@ -26,12 +26,12 @@ import numpy as np
 
 from .frsvt import frsvt
 from .linalg import norm2_power
-from .svt import soft_shrink, svt_exact
+from .svt import soft_shrink, svt_exact, wsvt_exact
 
 
 def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
               mu_max_factor=1e7, norm2=None, L0=None, backend="frsvt",
-              record_states=False, ap=None, varsigma_alpha=None):
+              record_states=False, ap=None, varsigma_alpha=None, keep=0, carry0=None):
     """Returns dict with L, E, Y, mu and per-iteration history.
 
     omega_fn(k) -> Omega (n x l) for iteration k (call index k).
@@ -43,6 +43,11 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
     first ones of Omega), and l_{k+1} follows Eq. (7). hist["l"] records l_k.
     varsigma_alpha: record hist["varsigma"], the Prop. 4 estimate of each
     call's sketch.
+    keep: partial SVT (Type B, PSVT of [30] replaced by FRSVT with the
+    partial thresholding P:645): thresholds t_i = 0 for the first `keep`
+    singular values, 1/mu after (the truncated nuclear norm sum_{i>keep} sigma_i).
+    carry0: the carried basis Q~ the first FRSVT call starts from (the basis
+    transfer between semi-online windows).
     """
     D = np.asarray(D, dtype=np.float64)
     m, n = D.shape
@@ -59,7 +64,7 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
     E = np.zeros_like(D)
     T = np.empty_like(D)     # scratch: D - L + Y/mu, then D - L - E
     Ymu = np.empty_like(D)   # Y / mu
-    carry = None
+    carry = None if carry0 is None else np.array(carry0, dtype=np.float64)
     hist = dict(r=[], s=[], resid=[], nrmse=[], mu=[], l=[], varsigma=[])
     l_cur = l
     if ap is not None:
@@ -80,7 +85,11 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
         soft_shrink_into(T, lam / mu, E)
         Aop = np.subtract(D, E, out=T)
         Aop += Ymu
-        if backend == "exact":
+        if backend == "exact" and keep > 0:
+            L, _, r = wsvt_exact(Aop, np.concatenate([np.zeros(keep), np.full(min(m, n) - keep, 1.0 / mu)]))
+            s = min(m, n)
+            new_carry = None
+        elif backend == "exact":
             L, _, r = svt_exact(Aop, 1.0 / mu)
             s = min(m, n)
             new_carry = None
@@ -96,7 +105,11 @@ def rpca_ialm(D, n_iter, l, q, omega_fn, rp=True, lam=None, mu0=None, rho=1.5,
                 nfresh = l_cur - r_c if (rp and r_c > 0) else l_cur
                 hist["varsigma"].append(sketch_varsigma(Aop, np.asarray(Om)[:, :max(nfresh, 1)],
                                                         carry if (rp and r_c > 0) else None, varsigma_alpha))
-            res = frsvt(Aop, Om, l_cur, q, tau=1.0 / mu, carry=carry, rp=rp)
+            if keep > 0:
+                w = np.concatenate([np.zeros(min(keep, l_cur)), np.full(max(l_cur - keep, 0), 1.0 / mu)])
+                res = frsvt(Aop, Om, l_cur, q, w=w, carry=carry, rp=rp)
+            else:
+                res = frsvt(Aop, Om, l_cur, q, tau=1.0 / mu, carry=carry, rp=rp)
             L, r, s, new_carry = res.X, res.r, res.s, res.carry
             del res
         hist["l"].append(l_cur)
@@ -133,6 +146,34 @@ def _fro_diff(X, Y, block=1024):
     for j in range(0, X.shape[1], block):
         acc += float(np.sum((X[:, j:j + block] - Y[:, j:j + block]) ** 2))
     return float(np.sqrt(acc))
+
+
+def rpca_windows(D, window, n_iter, l, q, omega_fn, keep=1, rho=1.5, transfer=True, L0=None):
+    """Semi-online Type-B RPCA over consecutive windows of `window` columns
+    (frames) of D: each window is an iALM solve with the
+    partial SVT (`keep` leading singular values unthresholded), and the
+    carried basis of one window's last FRSVT call starts the next window's
+    first call (basis transfer; transfer=False starts every window fresh).
+    lambda = 1/sqrt(max(m, window)) per window. Returns the per-window
+    outputs (L, E, hist, norm2) and the stitched L, E."""
+    D = np.asarray(D, dtype=np.float64)
+    m, N = D.shape
+    assert N % window == 0, "the frames must fill whole windows"
+    outs, carry = [], None
+    L = np.zeros_like(D)
+    E = np.zeros_like(D)
+    for w in range(N // window):
+        cols = slice(w * window, (w + 1) * window)
+        Dw = np.ascontiguousarray(D[:, cols])
+        n2 = norm2_power(Dw)
+        out = rpca_ialm(Dw, n_iter, l, q, omega_fn, rp=True, rho=rho, norm2=n2, keep=keep,
+                        carry0=carry if transfer else None,
+                        L0=None if L0 is None else np.ascontiguousarray(L0[:, cols]))
+        L[:, cols] = out["L"]
+        E[:, cols] = out["E"]
+        carry = out["carry"]
+        outs.append(dict(L=out["L"], E=out["E"], hist=out["hist"], norm2=n2, carry=carry))
+    return dict(L=L, E=E, windows=outs)
 
 
 def reweighted_wsvt(A, n_calls, l, q, C, eps, omega_fn, rp=True):

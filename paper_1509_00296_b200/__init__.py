@@ -175,7 +175,8 @@ class Frsvt:
                                                   ctypes.byref(res) if want_resid else None))
         return res.value if want_resid else None
 
-    def rpca_state(self, D, E, A, L=None, lam=0.0, rho=1.5, mu_max_factor=1e7, norm2_D=0.0, mu0=0.0):
+    def rpca_state(self, D, E, A, L=None, lam=0.0, rho=1.5, mu_max_factor=1e7, norm2_D=0.0, mu0=0.0, keep=0,
+                   transfer=False):
         ld = _ld(D, self.m, self.dtype, "D")
         for t, nm in ((E, "E"), (A, "A")) + (((L, "L"),) if L is not None else ()):
             if _ld(t, self.m, self.dtype, nm) != ld:
@@ -192,6 +193,8 @@ class Frsvt:
         st.norm2_D = float(norm2_D)
         st.mu0 = float(mu0)
         st.iter = 0
+        st.keep = int(keep)
+        st.transfer = 1 if transfer else 0
         st._keep = (D, E, A, L)
         return st
 

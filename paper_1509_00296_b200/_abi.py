@@ -42,7 +42,8 @@ class RpcaState(ctypes.Structure):
     _fields_ = [("D", ctypes.c_void_p), ("E", ctypes.c_void_p), ("A", ctypes.c_void_p),
                 ("L", ctypes.c_void_p), ("ld", ctypes.c_int64), ("lambda_", ctypes.c_double),
                 ("rho", ctypes.c_double), ("mu_max_factor", ctypes.c_double),
-                ("norm2_D", ctypes.c_double), ("mu0", ctypes.c_double), ("iter", ctypes.c_int32)]
+                ("norm2_D", ctypes.c_double), ("mu0", ctypes.c_double), ("iter", ctypes.c_int32),
+                ("keep", ctypes.c_int32), ("transfer", ctypes.c_int32)]
 
 
 def load_library(path=LIB_PATH):

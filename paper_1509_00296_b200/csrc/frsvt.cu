@@ -121,6 +121,7 @@ struct frsvt_handle {
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_OPT_FUSED_SKETCH)
   int ap_on, ap_a, ap_jump, ap_b, ap_l0;  // adaptive rank prediction (Eq. 7), frsvt_set_adaptive_rank
+  int keep;          // partial SVT of the current rpca step (rpca_state.keep; 0 for frsvt_apply*)
   double* resid_out;  // where the next sketch orthonormalisation reports its last-sample residual
   bool fs_armed;     // the last composition may have formed Y_p for the next call (dev->fs_done)
   float* fspart;     // fused-sketch partial rows, one 24 x 128 block per composition CTA
@@ -1011,14 +1012,14 @@ frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const do
   if (h->t2_pending) {  // Mc = T2 (U_B)_K, Mp = T2 (U_B)_K diag(d/sigma)
     shrink_kernel<double><<<1, 1024, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec, C,
                                                 eps, h->dprev, &h->dev->have_prev, h->McD, h->MpD, &h->dev->r,
-                                                &h->dev->flags, h->dev->rep);
+                                                &h->dev->flags, h->dev->rep, h->keep);
     TRY(post_launch(h));
     TRY(gemm_ll<T>(h, h->T2d, 0, h->McD, 0, (T*)h->Mc));
     TRY(gemm_ll<T>(h, h->T2d, 0, h->MpD, 0, (T*)h->Mp));
   } else {
     shrink_kernel<T><<<1, 1024, 0, h->st>>>(h->sigma, h->UB, l, &h->dev->s, wmode, tau, tau_dev, h->wvec,
                                            C, eps, h->dprev, &h->dev->have_prev, (T*)h->Mc, (T*)h->Mp,
-                                           &h->dev->r, &h->dev->flags, h->dev->rep);
+                                           &h->dev->r, &h->dev->flags, h->dev->rep, h->keep);
     TRY(post_launch(h));
   }
   TRY(apply_fast<T>(h, (const T*)h->Q, h->m, true, (const T*)h->Mc, (T*)h->Qt));
@@ -1032,7 +1033,9 @@ frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, dou
   TRY(range_finder<T>(h, A, lda, h->q, 1000u, h->rp != 0, h->call));
   // exact early-out of the small SVD when every sigma is certified <= the
   // smallest threshold (scalar tau, or the smallest explicit weight)
-  if (wmode == 0) TRY(small_svd<T>(h, A, lda, tau_dev ? 2 : 1, tau, tau_dev));
+  // (partial SVT, keep > 0: t_min = 0, no shortcut and the standard Jacobi measure)
+  if (wmode == 0 && h->keep > 0) TRY(small_svd<T>(h, A, lda));
+  else if (wmode == 0) TRY(small_svd<T>(h, A, lda, tau_dev ? 2 : 1, tau, tau_dev));
   else if (wmode == 1) TRY(small_svd<T>(h, A, lda, 1, tau));
   else TRY(small_svd<T>(h, A, lda));
   TRY(shrink_and_factors<T>(h, wmode, tau, tau_dev, C, eps));
@@ -1120,6 +1123,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   T* E = (T*)st->E;
   T* A = (T*)st->A;
   CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  h->keep = st->keep;
   if (st->iter == 0) {
     // ---- init: norms, mu_0, Y_0, E_1, A_1 ----
     const int nb = grid1d(h->m * h->n);
@@ -1135,10 +1139,14 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
     TRY(post_launch(h));
     alm_init_kernel<T><<<nb, 256, 0, h->st>>>(D, E, A, h->m, h->n, st->ld, h->dev->mu, h->dev->scal, lambda);
     TRY(post_launch(h));
-    // fresh solve: empty carry, Omega sequence restarts at call 0
-    CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
+    // fresh solve: empty carry (unless the basis is transferred from the
+    // previous solve: the semi-online windows of P:645), Omega sequence
+    // restarts at call 0
+    if (!st->transfer) {
+      CK(cudaMemsetAsync(&h->dev->r, 0, sizeof(int), h->st));
+      CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
+    }
     CK(cudaMemsetAsync(&h->dev->have_prev, 0, sizeof(int), h->st));
-    CK(cudaMemsetAsync(h->Qt, 0, (size_t)h->m * h->l * h->esz, h->st));
     if (h->ap_on) {
       ap_reset_kernel<<<1, 32, 0, h->st>>>(h->dev, h->ap_l0);
       TRY(post_launch(h));
@@ -1488,6 +1496,7 @@ frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau
                          frsvt_info* info) {
   if (h) h->fs_armed = false;  // a fused next sketch belongs to rpca_alm_step
   if (!h || !A || !X || lda < h->m || ldx < h->m || !(tau >= 0) || !std::isfinite(tau)) return FRSVT_EINVAL;
+  h->keep = 0;
   if (!rank_uniform_layout(h, A, lda)) return FRSVT_EINVAL;
   if (h->cfg.dtype == FRSVT_F32) return apply_impl<float>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
   return apply_impl<double>(h, A, lda, 0, tau, nullptr, 0, 0, X, ldx, info);
@@ -1499,6 +1508,7 @@ frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda, i
   if (h) h->fs_armed = false;
   if (!h || !A || !X || lda < h->m || ldx < h->m) return FRSVT_EINVAL;
   if (!rank_uniform_layout(h, A, lda)) return FRSVT_EINVAL;
+  h->keep = 0;
   int km;
   if (wmode == 0) {
     if (!w) return FRSVT_EINVAL;
@@ -1518,6 +1528,8 @@ frsvt_status frsvt_apply_weighted(frsvt_handle* h, const void* A, int64_t lda, i
 frsvt_status rpca_alm_step(frsvt_handle* h, rpca_state* st, int32_t finalize, double* rel_resid) {
   if (!h || !st || !st->D || !st->E || !st->A || st->ld < h->m) return FRSVT_EINVAL;
   if (finalize && !st->L) return FRSVT_EINVAL;
+  if (st->keep < 0 || st->keep > h->l || (st->transfer != 0 && st->transfer != 1) || (st->transfer && !h->rp))
+    return FRSVT_EINVAL;
   if (!(st->rho > 1.0) || !std::isfinite(st->rho)) return FRSVT_EINVAL;
   if (st->iter < 0) return FRSVT_EINVAL;
   if (st->iter == 0 && !(st->mu_max_factor >= 1.0)) return FRSVT_EINVAL;

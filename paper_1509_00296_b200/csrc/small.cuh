@@ -116,7 +116,9 @@ __global__ void shrink_kernel(const double* __restrict__ sigma, const double* __
                               const double* __restrict__ tau_dev, const double* __restrict__ w,
                               double C, double eps, double* __restrict__ d_prev, int* have_prev,
                               Tq* __restrict__ Mc, Tq* __restrict__ Mp, int* __restrict__ r_dev,
-                              int* __restrict__ flags, double* __restrict__ rep) {
+                              int* __restrict__ flags, double* __restrict__ rep, int keep = 0) {
+  // keep (wmode 0): partial SVT, the first `keep` singular values are not
+  // thresholded (t_i = 0, the truncated nuclear norm of Type B)
   __shared__ double d_sh[FRSVT_LMAX], f_sh[FRSVT_LMAX];
   __shared__ int kept[FRSVT_LMAX];
   __shared__ int r_sh;
@@ -126,7 +128,7 @@ __global__ void shrink_kernel(const double* __restrict__ sigma, const double* __
   for (int i = tid; i < l; i += blockDim.x) {
     const double sg = sigma[i];
     double t;
-    if (wmode == 0) t = tau_dev ? *tau_dev : tau;
+    if (wmode == 0) t = i < keep ? 0.0 : (tau_dev ? *tau_dev : tau);
     else if (wmode == 1) t = w[i];
     else if (wmode == 3 && prev_ok) t = C / (d_prev[i] + eps);
     else t = C / (sg + eps);
