@@ -104,6 +104,22 @@ typedef struct {
 
 typedef struct frsvt_handle frsvt_handle;
 
+/* Batched FRSVT of `batch` independent small fp32 matrices (SURVEY.md §8(f)
+ * NEXT-3; WNNM patch groups P:23/P:48, per-window problems P:643): one CTA per
+ * matrix runs Algorithm 1 (no range propagation) in shared memory; one
+ * launch, no handle. Matrix b is A + b strideA (m x n, column-major, leading
+ * dim lda), its result X + b strideX (ldx); all device pointers. Omega: n x l
+ * (ldo), shared by the batch. 1 <= l <= min(16, m, n), 0 <= q <= 16, and
+ * 8 ((m + n) l + l^2 + 192) + 4 m n bytes of shared memory <= 227 KB.
+ * wmode 0: t_i = tau, or tau_batch[b] (device, nullable); wmode 1: t_i = w[i]
+ * (device, l values, by descending rank position). Outputs (device,
+ * nullable): r_out[b] kept rank, sigma_out[b l + i] singular values of
+ * B = Q^T A, descending. Enqueued on cuda_stream; returns before completion. */
+frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const float* A,
+                                 int64_t lda, int64_t strideA, const float* Omega, int64_t ldo, int32_t wmode,
+                                 double tau, const double* tau_batch, const double* w, float* X, int64_t ldx,
+                                 int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream);
+
 /* Loopback process group of `nranks` (2..FRSVT_LOOPBACK_MAX) virtual ranks:
  * the row-sharded path on ONE device and in ONE process,
  * each rank a handle created with cfg.group = this group, driven by its own

@@ -16,7 +16,7 @@ import torch
 from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, FrsvtConfig, FrsvtInfo,
                    RpcaState, load_library, status_string)
 
-__all__ = ["Frsvt", "FrsvtError", "LoopbackGroup", "lib", "library_path", "colmajor", "W_EXPLICIT",
+__all__ = ["Frsvt", "FrsvtError", "LoopbackGroup", "batched_apply", "lib", "library_path", "colmajor", "W_EXPLICIT",
            "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH"]
 
 W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
@@ -52,6 +52,49 @@ def _ld(x, rows, dtype, name):
     if x.stride(0) != 1 or x.stride(1) < max(1, rows):
         raise ValueError("%s must be column-major (stride (1, ld>=rows)), got %s" % (name, x.stride()))
     return x.stride(1)
+
+
+def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None):
+    """frsvt_batched_apply: X[b] = FRSVT(A[b]) for a batch of small fp32
+    matrices (one CTA each). A: (batch, m, n) CUDA fp32 with each matrix
+    column-major (A[b].stride() == (1, ld)); Omega: n x l column-major. tau: a
+    float or a (batch,) tensor; w: (l,) weights. Returns X (batch, m, n, same
+    layout), r (batch,) int32, sigma (batch, l) float64."""
+    if A.dim() != 3 or A.dtype != torch.float32 or A.device.type != "cuda":
+        raise ValueError("A must be a (batch, m, n) CUDA fp32 tensor")
+    batch, m, n = A.shape
+    if batch == 0:
+        l = Omega.shape[1]
+        return (torch.empty((0, m, n), dtype=torch.float32, device=A.device),
+                torch.empty(0, dtype=torch.int32, device=A.device),
+                torch.empty((0, l), dtype=torch.float64, device=A.device))
+    if A.stride(1) != 1:
+        raise ValueError("each A[b] must be column-major")
+    lda, sA = A.stride(2), A.stride(0)
+    Om = colmajor(Omega.to(device=A.device, dtype=torch.float32))
+    l = Om.shape[1]
+    X = torch.empty((batch, n, m), dtype=torch.float32, device=A.device).transpose(1, 2)
+    r = torch.empty(batch, dtype=torch.int32, device=A.device)
+    sig = torch.empty((batch, l), dtype=torch.float64, device=A.device)
+    wmode, tau_s, tau_p, w_p = 0, 0.0, None, None
+    if w is not None:
+        wmode = 1
+        wt = torch.as_tensor(w, dtype=torch.float64, device=A.device).contiguous()
+        w_p = ctypes.c_void_p(wt.data_ptr())
+    elif torch.is_tensor(tau):
+        tt = tau.to(device=A.device, dtype=torch.float64).contiguous()
+        tau_p = ctypes.c_void_p(tt.data_ptr())
+    else:
+        tau_s = float(tau)
+    st = stream if stream is not None else torch.cuda.current_stream()
+    for t in (A, Om) + ((wt,) if w is not None else ()) + ((tt,) if tau_p is not None else ()):
+        t.record_stream(st)  # kept alive for the asynchronous kernel on `st`
+    _check("frsvt_batched_apply", lib.frsvt_batched_apply(
+        int(batch), int(m), int(n), int(l), int(q), ctypes.c_void_p(A.data_ptr()), int(lda), int(sA),
+        ctypes.c_void_p(Om.data_ptr()), int(Om.stride(1)), wmode, tau_s, tau_p, w_p, ctypes.c_void_p(X.data_ptr()),
+        int(X.stride(2)), int(X.stride(0)), ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(sig.data_ptr()),
+        ctypes.c_void_p(st.cuda_stream)))
+    return X, r, sig
 
 
 class LoopbackGroup:

@@ -27,6 +27,7 @@
 #include "tc_util.cuh"
 #include "tc_compose2.cuh"
 #include "tc_pass3.cuh"
+#include "batched.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -1266,6 +1267,32 @@ const char* frsvt_status_string(frsvt_status s) {
     case FRSVT_ENOMEM: return "out of device memory";
   }
   return "unknown status";
+}
+
+frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const float* A,
+                                 int64_t lda, int64_t strideA, const float* Omega, int64_t ldo, int32_t wmode,
+                                 double tau, const double* tau_batch, const double* w, float* X, int64_t ldx,
+                                 int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream) {
+  if (batch < 0 || m < 1 || n < 1 || l < 1 || l > BT_LMAX || l > m || l > n || q < 0 || q > 16) return FRSVT_EINVAL;
+  if (lda < m || ldx < m || ldo < n || strideA < lda * n || strideX < ldx * n) return FRSVT_EINVAL;
+  if (batch == 0) return FRSVT_OK;  // nothing to do (the pointers may be NULL)
+  if (!A || !Omega || !X) return FRSVT_EINVAL;
+  if (wmode == 0) {
+    if (!tau_batch && (!(tau >= 0) || !std::isfinite(tau))) return FRSVT_EINVAL;
+  } else if (wmode == 1) {
+    if (!w) return FRSVT_EINVAL;
+  } else {
+    return FRSVT_EINVAL;
+  }
+  const size_t smem = batched_smem_bytes((int)m, (int)n, l);
+  if (smem > 227 * 1024 || m > (1 << 20) || n > (1 << 20)) return FRSVT_EINVAL;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CK(cudaFuncSetAttribute(batched_frsvt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  batched_frsvt_kernel<<<(unsigned)batch, BT_THREADS, smem, st>>>((int)m, (int)n, l, q, A, lda, strideA, Omega, ldo,
+                                                                    wmode, tau, tau_batch, w, X, ldx, strideX, r_out,
+                                                                    sigma_out);
+  CK(cudaGetLastError());
+  return FRSVT_OK;
 }
 
 frsvt_status frsvt_loopback_create(int32_t nranks, frsvt_group** out) {
