@@ -27,7 +27,7 @@ def nvcc_cmd(out=LIB, extra=()):
     return ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
             "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"), "-I", inc,
-            *SOURCES, "-o", out, "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib,
+            *SOURCES, "-o", out, "-L", lib, "-l:libnccl.so.2", "-ldl", "-Xlinker", "-rpath=" + lib,
             *extra]
 
 

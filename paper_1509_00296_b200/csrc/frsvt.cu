@@ -31,6 +31,7 @@
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <condition_variable>
@@ -194,6 +195,13 @@ namespace {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// NVTX range over one phase of the path (host-side markers for nsys/ncu
+// timelines: range finder, small SVD, shrink/factors, composition/epilogue)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 frsvt_status post_launch(frsvt_handle* h) {
   h->launches++;
   CK(cudaGetLastError());
@@ -334,7 +342,7 @@ bool make_map(CUtensorMap* map, const float* ptr, uint64_t dim0, uint64_t dim1, 
 }
 
 bool tc_eligible(const frsvt_handle* h, const void* A, int64_t lda) {
-  return h->use_tc && h->esz == 4 && h->l >= 16 && (lda % 4) == 0 && ((uintptr_t)A % 16) == 0;
+  return h->use_tc && h->esz == 4 && (lda % 4) == 0 && ((uintptr_t)A % 16) == 0;
 }
 
 int tc_np(int l) { return l <= 32 ? 32 : (l <= 64 ? 64 : 128); }
@@ -433,6 +441,9 @@ frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap
   const int64_t units = talign ? mgroups : total;
   const int G = (int)(units < Gmax ? units : Gmax);
   if (mtiles > h->ncnt) return FRSVT_EINVAL;  // the tile counters cover every row tile (sized at create)
+  // tiles shared by many clusters (few output tiles): the slots are summed by
+  // a separate many-block kernel instead of the last covering CTA
+  const bool sep_fix = !talign && (int64_t)G > 4 * mgroups;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(G * CL));
   lc.blockDim = dim3(tc::P3_THREADS);
@@ -446,7 +457,11 @@ frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap
   lc.attrs = at;
   lc.numAttrs = 1;
   CK(cudaLaunchKernelEx(&lc, tc::tc_pass3_kernel<MODE, NP, TERMS>, mA, mBh, mBx, Mtot, Ktot, h->l, out, ldo, add,
-                        ldadd, h->skpart, rp_dev, dbg, h->tilecnt, skip_dev));
+                        ldadd, h->skpart, rp_dev, dbg, sep_fix ? nullptr : h->tilecnt, skip_dev));
+  TRY(post_launch(h));
+  if (!sep_fix) return FRSVT_OK;
+  tc::p3_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)h->l), 128, 0, h->st>>>(
+      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev, skip_dev);
   return post_launch(h);
 }
 
@@ -511,7 +526,7 @@ frsvt_status tc_pass3(frsvt_handle* h, const float* A, int64_t lda, int64_t Mtot
 // in frsvt_create and agreed over the ranks (h->tc_m): every rank must take the
 // same orthonormalisation route, or the replicated factors would differ.
 bool tc_small_local(const frsvt_handle* h, int64_t rows) {
-  return h->use_tc && h->esz == 4 && h->l >= 16 && (rows % 4) == 0 && rows >= 128;
+  return h->use_tc && h->esz == 4 && (rows % 4) == 0 && rows >= 128;
 }
 bool tc_small_ok(const frsvt_handle* h, int64_t rows, bool m_rows) {
   return m_rows ? h->tc_m != 0 : tc_small_local(h, rows);
@@ -676,14 +691,19 @@ frsvt_status gram(frsvt_handle* h, const T* Y, int64_t rows, int64_t ld, bool sh
   const int l = h->l;
   // fp64 tensor cores (DMMA), upper 8x8 blocks only (gram_dmma.cuh); one wave
   // (1 CTA of 512 threads per SM at 128 registers), >= 32 rows each
-  int S = (int)cdiv(rows, GD_ROWS);
+  const bool narrow = l <= GS_LMAX && rows >= 32768;  // tall and narrow: entries per thread (gram_small_kernel)
+  const int CR = narrow ? GS_ROWS : GD_ROWS;
+  int S = (int)cdiv(rows, CR);
   const int Smax = (int)(h->partd_elems / ((size_t)l * l));
   if (S > h->nsm) S = h->nsm;
   if (S > Smax) S = Smax;
   if (S < 1) S = 1;
-  const int64_t rpc = cdiv(cdiv(rows, S), GD_ROWS) * GD_ROWS;
+  const int64_t rpc = cdiv(cdiv(rows, S), CR) * CR;
   S = (int)cdiv(rows, rpc);
-  gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd, r_dev);
+  if (narrow)  // (RP: all blocks are formed; chol_inv reads only the ones it needs)
+    gram_small_kernel<T><<<S, GS_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd);
+  else
+    gram_dmma_kernel<T><<<S, GD_THREADS, 0, h->st>>>(Y, rows, ld, l, rpc, h->partd, r_dev);
   TRY(post_launch(h));
   splitk_reduce_wide_kernel<double, double><<<(unsigned)cdiv((int64_t)l * l, 32), 256, 0, h->st>>>(h->partd, S, l, l,
                                                                                                    h->G, l);
@@ -1031,7 +1051,11 @@ frsvt_status shrink_and_factors(frsvt_handle* h, int wmode, double tau, const do
 template <typename T>
 frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, double tau,
                         const double* tau_dev, double C, double eps) {
-  TRY(range_finder<T>(h, A, lda, h->q, 1000u, h->rp != 0, h->call));
+  {
+    NvtxRange nv("frsvt.range_finder");
+    TRY(range_finder<T>(h, A, lda, h->q, 1000u, h->rp != 0, h->call));
+  }
+  NvtxRange nv("frsvt.small_svd+shrink");
   // exact early-out of the small SVD when every sigma is certified <= the
   // smallest threshold (scalar tau, or the smallest explicit weight)
   // (partial SVT, keep > 0: t_min = 0, no shortcut and the standard Jacobi measure)
@@ -1051,6 +1075,7 @@ frsvt_status frsvt_core(frsvt_handle* h, const T* A, int64_t lda, int wmode, dou
 // X = Q~ Wt^T  (reconstruction, K = r)
 template <typename T>
 frsvt_status compose_X(frsvt_handle* h, T* X, int64_t ldx) {
+  NvtxRange nv("frsvt.compose");
   if constexpr (sizeof(T) == 4) {
     if (h->use_tc) {
       TRY(prof_begin(h));
@@ -1159,6 +1184,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   TRY(post_launch(h));
   TRY(frsvt_core<T>(h, A, st->ld, 0, 0.0, &h->dev->tau, 0.0, 0.0));
   // fused reconstruction + iALM epilogue (one pass over D, A, E)
+  NvtxRange nv("rpca.epilogue");
   int nparts = (int)(cdiv(h->m, 128) * cdiv(h->n, 128));
   TRY(prof_begin(h));
   bool done = false;

@@ -32,7 +32,8 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
   // r_dev (nullable, range propagation): only the 8 x 8 blocks whose column
   // block reaches the fresh columns [r, l) are formed (G12 and G22, the
   // entries chol_inv_kernel reads); the rest of the partial is left stale.
-  __shared__ double sY[GD_ROWS * GD_LD];
+  constexpr int CR = GD_ROWS, LDC = GD_LD;
+  __shared__ double sY[CR * LDC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb8 = (l + 7) >> 3;
   const int nblk = nb8 * (nb8 + 1) / 2;
@@ -63,31 +64,31 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
   const int kq = lane & 3, g = lane >> 2;
   // software pipeline: the next 32-row chunk is loaded into registers while
   // the current one is multiplied (all of a thread's loads in flight at once)
-  constexpr int PER = GD_ROWS * FRSVT_LMAX / GD_THREADS;  // 8 elements per thread
+  constexpr int PER = CR * (LDC - 4) / GD_THREADS;  // 8 elements per thread
   Tin pre[PER];
   auto load_chunk = [&](int64_t rc) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int idx = threadIdx.x + GD_THREADS * u;
-      const int rr = idx & (GD_ROWS - 1), c = idx >> 5;
+      const int rr = idx % CR, c = idx / CR;
       const int64_t r = rc + rr;
       pre[u] = (c < l && r < r1) ? Y[r + (int64_t)c * ldy] : Tin(0);
     }
   };
   if (r0 < r1) load_chunk(r0);
-  for (int64_t rc = r0; rc < r1; rc += GD_ROWS) {
+  for (int64_t rc = r0; rc < r1; rc += CR) {
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int idx = threadIdx.x + GD_THREADS * u;
-      const int rr = idx & (GD_ROWS - 1), c = idx >> 5;
-      sY[rr * GD_LD + c] = (double)pre[u];  // columns >= l are zero (padding of the last 8-block)
+      const int rr = idx % CR, c = idx / CR;
+      sY[rr * LDC + c] = (double)pre[u];  // columns >= l are zero (padding of the last 8-block)
     }
     __syncthreads();
-    if (rc + GD_ROWS < r1) load_chunk(rc + GD_ROWS);
+    if (rc + CR < r1) load_chunk(rc + CR);
 #pragma unroll 2
-    for (int k = 0; k < GD_ROWS; k += 4) {
-      const double* rowp = sY + (k + kq) * GD_LD + g;
+    for (int k = 0; k < CR; k += 4) {
+      const double* rowp = sY + (k + kq) * LDC + g;
 #pragma unroll
       for (int t = 0; t < GD_MAXB; ++t) {
         if (bi[t] >= 0) {
@@ -113,6 +114,62 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
         P[j + (int64_t)i * l] = v;
       }
     }
+  }
+}
+
+// Gram of a tall NARROW matrix (l <= 16, e.g. BASELINE c3's l = 10 over
+// 76800 rows): the 8 x 8 DMMA blocks would leave most warps idle and chain
+// dependent MMAs, so here every thread owns entries (i <= j) of the upper
+// triangle and accumulates them in fp64 over 256-row chunks staged in shared
+// memory (4 independent partial sums per entry); one partial per CTA (both
+// triangles), summed over CTAs by splitk_reduce_wide_kernel.
+constexpr int GS_THREADS = 256;
+constexpr int GS_ROWS = 256;
+constexpr int GS_LMAX = 16;
+template <typename Tin>
+__global__ void __launch_bounds__(GS_THREADS)
+gram_small_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, int64_t rows_per_cta,
+                  double* __restrict__ part) {
+  __shared__ double sY[GS_LMAX * GS_ROWS];  // column-major chunk
+  const int ne = l * (l + 1) / 2;
+  // entry of this thread (l <= 16: at most 136 entries)
+  int ei = threadIdx.x, ii = 0, jj = 0;
+  if (ei < ne) {
+    int q = ei;
+    while (q >= l - ii) {
+      q -= l - ii;
+      ++ii;
+    }
+    jj = ii + q;
+  }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int64_t r0 = blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  for (int64_t rc = r0; rc < r1; rc += GS_ROWS) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < GS_ROWS * l; idx += GS_THREADS) {
+      const int rr = idx % GS_ROWS, c = idx / GS_ROWS;
+      const int64_t r = rc + rr;
+      sY[c * GS_ROWS + rr] = r < r1 ? (double)Y[r + (int64_t)c * ldy] : 0.0;
+    }
+    __syncthreads();
+    if (ei < ne) {
+      const double* yi = sY + ii * GS_ROWS;
+      const double* yj = sY + jj * GS_ROWS;
+#pragma unroll 4
+      for (int k = 0; k < GS_ROWS; k += 4) {
+        a0 = fma(yi[k], yj[k], a0);
+        a1 = fma(yi[k + 1], yj[k + 1], a1);
+        a2 = fma(yi[k + 2], yj[k + 2], a2);
+        a3 = fma(yi[k + 3], yj[k + 3], a3);
+      }
+    }
+  }
+  if (ei < ne) {
+    const double v = (a0 + a1) + (a2 + a3);
+    double* P = part + (int64_t)blockIdx.x * l * l;
+    P[ii + (int64_t)jj * l] = v;
+    P[jj + (int64_t)ii * l] = v;
   }
 }
 

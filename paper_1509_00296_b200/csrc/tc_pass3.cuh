@@ -488,8 +488,10 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
           for (int j = 0; j < HALF; ++j) p[(int64_t)(col0 + j) * 128 + row] = sum[j];
           // covering clusters of this work tile, and whether this CTA is the last to finish
+          // (tile_cnt == nullptr: p3_fixup_kernel sums the slots after the pass)
           __shared__ int s_last;
           __shared__ int s_c0, s_c1;
+          if (tile_cnt) {
           __threadfence();
           asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 flush warps
           if (warp == 12 && lane == 0) {
@@ -538,6 +540,7 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
               }
             }
           }
+          }  // tile_cnt
         }
 #pragma unroll
         for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
@@ -552,6 +555,72 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     tc_fence_after();
     tmem_dealloc_cg2(tbase, 512);
   }
+}
+
+// Tiles split between MANY clusters (a pass with few output tiles, e.g. the
+// A^T Q of a tall matrix with a narrow n): out = sum of the covering CTAs'
+// partial slots in cluster order (+ add), one block per (row tile, 8-column
+// group) so the reduction runs on many SMs instead of in the last covering
+// CTA. Same slots, order and result as the in-kernel fixup. Grid (row
+// tiles, output columns), 128 threads (one per row).
+template <int NP>
+__global__ void __launch_bounds__(128) p3_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
+                                                       const float* __restrict__ part, float* __restrict__ out,
+                                                       int64_t ldo, const float* __restrict__ add, int64_t ldadd,
+                                                       const int* __restrict__ rp_dev,
+                                                       const int* __restrict__ skip_dev) {
+  if (skip_dev && *skip_dev) return;  // the pass was skipped: nothing to sum
+  constexpr int CL = 2;
+  __shared__ int64_t soff[256];
+  __shared__ int ncov;
+  const int nch = (Ktot + BK - 1) / BK;
+  const int mtiles = (Mtot + 127) / 128;
+  const int mgroups = (mtiles + CL - 1) / CL;
+  const int64_t total = (int64_t)mgroups * nch;
+  const int tile = blockIdx.x;
+  const int wt = tile / CL, crank = tile % CL;
+  if (threadIdx.x == 0) {
+    const int64_t t0 = (int64_t)wt * nch, t1 = t0 + nch;
+    int c0 = (int)((t0 * G) / total);
+    while (c0 > 0 && sk_range_begin(total, G, c0) > t0) --c0;
+    while (sk_range_begin(total, G, c0 + 1) <= t0) ++c0;
+    int c1 = c0;
+    while (c1 + 1 < G && sk_range_begin(total, G, c1 + 1) < t1) ++c1;
+    const bool whole = (c0 == c1) && sk_range_begin(total, G, c0) <= t0 && sk_range_begin(total, G, c0 + 1) >= t1;
+    int k = 0;
+    if (!whole) {
+      for (int cc = c0; cc <= c1 && k < 256; ++cc) {
+        const int64_t b = sk_range_begin(total, G, cc);
+        if (sk_range_begin(total, G, cc + 1) <= b) continue;
+        soff[k++] = ((int64_t)(cc * CL + crank) * P3_SLOTS + ((b >= t0) ? 0 : 1)) * 128 * NP;
+      }
+    }
+    ncov = k;
+  }
+  __syncthreads();
+  const int nc = ncov;
+  if (nc == 0) return;  // written directly by the pass
+  const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
+  const int c = blockIdx.y;  // one output column per block, one row per thread
+  const int row = threadIdx.x, gm = tile * 128 + row;
+  if (gm >= Mtot || row >= 128) return;
+  if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
+    if (add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+    return;
+  }
+  const float* base = part + (int64_t)(c - rsh) * 128 + row;
+  float acc = 0.f;
+  int k = 0;
+  for (; k + 8 <= nc; k += 8) {  // 8 independent loads in flight, summed in slot order
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + soff[k + u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; k < nc; ++k) acc += __ldcg(base + soff[k]);
+  if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
+  out[gm + (int64_t)c * ldo] = acc;
 }
 
 // B operand split of a TERMS = 2 pass: Bh = rna_tf32(x) (fp32, ld ldh) and

@@ -146,8 +146,10 @@ def test_c5_full_solve_against_cached_oracle(P):
     # crosses the spectrum (SURVEY §8(c) protocol 3: at most 2 iterations)
     assert sum(a != b for a, b in zip(r_gpu, ref["r"])) <= 2, (r_gpu, ref["r"])
     assert r_gpu[-1] == ref["r"][-1]
-    for k in (0, 10, 20, 30, 39):
-        assert abs(res[k] - ref["resid"][k]) <= 1e-3 * ref["resid"][k] + 2e-7, (k, res[k], ref["resid"][k])
+    # the residual trajectory down to the fp32 floor of the tensor-core products
+    # (~1e-6 relative, reading R5; the fp64 oracle goes on to ~1e-12)
+    for k in (0, 10, 14, 15, 16, 20, 30, 39):
+        assert abs(res[k] - ref["resid"][k]) <= 1e-3 * ref["resid"][k] + 1e-5, (k, res[k], ref["resid"][k])
     ii = torch.tensor(ref["sample_rows"], device="cuda")
     jj = torch.tensor(ref["sample_cols"], device="cuda")
     Ls = L[ii, jj].double().cpu().numpy()

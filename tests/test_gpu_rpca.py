@@ -52,8 +52,9 @@ def test_rpca_free_running(P, name, over):
     nrmse_o = ref["hist"]["nrmse"][-1]
     assert abs(nrmse_g - nrmse_o) <= 1e-3
     assert np.linalg.norm(Lg - ref["L"]) <= 1e-3 * np.linalg.norm(ref["L"])
-    # residual reaches the textbook value or the fp32 floor (~u32 * sqrt(mn) relative)
-    assert resid[-1] <= max(10 * ref["hist"]["resid"][-1], 2e-7)
+    # residual reaches the textbook value or the floor of the tensor-core
+    # products (fp32-level, ~1e-6 relative: reading R5)
+    assert resid[-1] <= max(10 * ref["hist"]["resid"][-1], 1e-6)
     assert np.linalg.norm(np64(E) - ref["E"]) <= 1e-3 * np.linalg.norm(ref["E"])
 
 

@@ -16,7 +16,7 @@ def P():
     return P
 
 
-@pytest.mark.parametrize("m,n,l", [(1036, 612, 16), (1036, 612, 37), (512, 1024, 64),
+@pytest.mark.parametrize("m,n,l", [(1036, 612, 4), (76800, 200, 10), (1036, 612, 16), (1036, 612, 37), (512, 1024, 64),
                                    (2048, 2056, 120), (4100, 260, 128), (130, 70000, 120), (40000, 300, 120)])
 @pytest.mark.parametrize("kind", [0, 1])
 def test_tc_pass_matches_fp64(P, m, n, l, kind):
