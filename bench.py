@@ -46,6 +46,17 @@ META = {
     "c5": dict(metric="RPCA-iALM iterations/s (FRSVT l=120, q=1, RP) on BASELINE c5", unit="iter/s"),
 }
 PASS_GATE = 0.70  # north_star: each pass over A at >= 70% of HBM at 1 GPU
+# FP64 FMA issue rate of one SM, measured on this pool's B200 (scripts/bt_phase.py:
+# 63.7 DFMA/clk per CTA from clock64, 148 x 1024 threads 34.8 TFLOP/s;
+# profiles/r2_fp64_rate.txt): the ALU roof of a one-CTA call (c1)
+DFMA_PER_CLK_SM = 64
+
+
+def _sm_max_mhz():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p)).get("sm_max_mhz", 1965.0))
+    return 1965.0
 
 
 def _peaks():
@@ -395,17 +406,26 @@ def run_ours(args, ws, rank, local, dist):
     live = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(live, key=lambda k: live[k][0])
     dms, dn, dbytes = live[dom]
-    achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9
     step_ms = ms_max / args.steps
+    bound, unit = "hbm", "GB/s"
+    if dom == "single":
+        # one CTA runs the whole call: the roof is that SM's FP64 FMA pipe
+        # (FLOPs 2 m n l (2q+3) per call, the library's kind-3 count)
+        bound, unit = "alu", "GFLOP/s"
+        peak = 2.0 * DFMA_PER_CLK_SM * _sm_max_mhz() / 1e3
+        peak_src = "one SM's FP64 FMA rate: %d DFMA/clk (measured) x 2 x %.0f MHz" % (DFMA_PER_CLK_SM, _sm_max_mhz())
+    achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9
     per_pass = {}
     for k, (pms, pn, pb) in live.items():
         gbs = pb / (pms / 1e3) / 1e9
         per_pass[k] = {"ms_per_step": pms / prof_steps, "launches_per_step": pn / prof_steps,
-                       "gbs": gbs, "frac": gbs / peak, "share_of_step": (pms / prof_steps) / step_ms}
-        if k != "compose":
+                       ("gflops" if k == "single" else "gbs"): gbs, "frac": gbs / peak,
+                       "share_of_step": (pms / prof_steps) / step_ms}
+        if k not in ("compose", "single"):
             per_pass[k]["meets_0p70_gate"] = gbs / peak >= PASS_GATE
     unit_bytes = alg_bytes_per_unit(cfg) * (W.m_loc / cfg.m)
     unit_gbs = unit_bytes * W.per_step / (step_ms / 1e3) / 1e9
+    hbm_peak = _peaks()[0]
     traffic, tensor_pct = _profile_facts(args.config, dom)
 
     # ---- end to end through the public API from pinned host memory -------
@@ -442,18 +462,19 @@ def run_ours(args, ws, rank, local, dist):
 
     if rank != 0:
         return None
-    kernel_names = {"AX": "tc_pass2_kernel<AX> (A X passes)", "AtQ": "tc_pass2_kernel<ATQ> (A^T Q passes)",
-                    "compose": "tc_compose2_kernel / composition (X or the fused iALM epilogue)"}
+    kernel_names = {"AX": "tc_pass3_kernel<AX> (A X passes)", "AtQ": "tc_pass3_kernel<ATQ> (A^T Q passes)",
+                    "compose": "tc_compose2_kernel / composition (X or the fused iALM epilogue)",
+                    "single": "batched_frsvt_kernel (the whole call in one CTA)"}
     return {"metric": META[args.config]["metric"], "value": value, "unit": META[args.config]["unit"],
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic (seeded Philox recipes of SURVEY §8(d))",
             "config": dict(_config_dict(cfg, ws, args.config), cuda_graph=graph is not None),
-            "roofline": {"bound": "hbm", "kernel": kernel_names.get(dom, dom), "kind": dom, "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "roofline": {"bound": bound, "kernel": kernel_names.get(dom, dom), "kind": dom, "achieved": achieved,
+                         "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
                          "tensor_pipe_pct": tensor_pct, "peak_source": peak_src,
                          "per_pass": per_pass, "pass_gate": PASS_GATE,
-                         "unit_algorithmic_bytes": unit_bytes, "unit_gbs": unit_gbs, "unit_frac": unit_gbs / peak,
+                         "unit_algorithmic_bytes": unit_bytes, "unit_gbs": unit_gbs, "unit_frac": unit_gbs / hbm_peak,
                          "per_pass_scope": ("one eager step right after the timed graph replays" if graph is not None
                                             else "all timed steps")},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}

@@ -62,6 +62,7 @@ typedef struct frsvt_group frsvt_group;
 #define FRSVT_FLAG_NONFINITE 1
 #define FRSVT_FLAG_NOCONV 2
 #define FRSVT_FLAG_NONMONOTONE_W 4
+#define FRSVT_FLAG_SINGLE_CTA 8   /* informational: frsvt_apply ran on the single-CTA path */
 
 typedef struct {
   int32_t dtype;            /* frsvt_dtype */
@@ -155,7 +156,12 @@ const char* frsvt_status_string(frsvt_status s);
  *   Q <- orth(A orth(A^T Q)), B = Q^T A, small SVD of B, shrink, compose.
  * A: m_local x n, leading dim lda >= m_local. X: m_local x n, ldx >= m_local,
  * may alias A (every read of A completes before X is written).
- * tau >= 0 finite. info: host, nullable (non-NULL synchronises). */
+ * tau >= 0 finite. info: host, nullable (non-NULL synchronises).
+ * A call small enough for one SM (no range propagation, one rank, l <= 16,
+ * m, n <= 1024 and A plus the small blocks within 227 KB of shared memory,
+ * e.g. BASELINE c1: 200 x 100 fp64) runs as ONE kernel launch (the
+ * batched design below with batch 1; info.flags has FRSVT_FLAG_SINGLE_CTA);
+ * explicit-weight calls of frsvt_apply_weighted take the same route. */
 frsvt_status frsvt_apply(frsvt_handle* h, const void* A, int64_t lda, double tau,
                          void* X, int64_t ldx, frsvt_info* info);
 
@@ -292,10 +298,12 @@ frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, v
 /* Pass profiling: with enable != 0 every kernel that streams the m x n
  * operand is bracketed by CUDA events on the handle's stream (enabling resets
  * the totals). kind: 0 = A*X passes (sketch, power), 1 = A^T*Q passes (power,
- * B), 2 = composition / fused iALM epilogue. Reading synchronises and returns
- * the summed event time (ms), the launch count and the algorithmic bytes of
- * those launches (m*n*elem per A pass; X write; 5 m*n*elem for the iALM
- * epilogue: D, A, E read, A, E written; 3 m*n*elem for a finalize step). */
+ * B), 2 = composition / fused iALM epilogue, 3 = single-CTA calls (the whole
+ * of Algorithm 1 in one kernel). Reading synchronises and returns the summed
+ * event time (ms), the launch count and the algorithmic bytes of those
+ * launches (m*n*elem per A pass; X write; 5 m*n*elem for the iALM epilogue:
+ * D, A, E read, A, E written; 3 m*n*elem for a finalize step) -- for kind 3
+ * the algorithmic FLOPs instead, 2 m n l (2q + 3) per call. */
 frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable);
 frsvt_status frsvt_profile_read(frsvt_handle* h, int32_t kind, double* ms, int64_t* launches, double* bytes);
 

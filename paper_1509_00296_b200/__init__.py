@@ -17,9 +17,12 @@ from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, Frs
                    RpcaState, load_library, status_string)
 
 __all__ = ["Frsvt", "FrsvtError", "LoopbackGroup", "batched_apply", "lib", "library_path", "colmajor", "W_EXPLICIT",
-           "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH"]
+           "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH", "FLAG_NONFINITE", "FLAG_NOCONV",
+           "FLAG_NONMONOTONE_W", "FLAG_SINGLE_CTA"]
 
 W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
+# frsvt_info.flags bits (include/frsvt.h FRSVT_FLAG_*)
+FLAG_NONFINITE, FLAG_NOCONV, FLAG_NONMONOTONE_W, FLAG_SINGLE_CTA = 1, 2, 4, 8
 
 lib, library_path = load_library()
 
@@ -386,9 +389,10 @@ class Frsvt:
         _check("frsvt_profile", lib.frsvt_profile(self._h, 1 if enable else 0))
 
     def profile_read(self):
-        """{kind: (ms, launches, bytes)} for kinds 'AX', 'AtQ', 'compose'."""
+        """{kind: (ms, launches, bytes)} for kinds 'AX', 'AtQ', 'compose', and
+        'single' (single-CTA calls; the third value is their FLOP count)."""
         out = {}
-        for k, name in enumerate(("AX", "AtQ", "compose")):
+        for k, name in enumerate(("AX", "AtQ", "compose", "single")):
             ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
             _check("frsvt_profile_read", lib.frsvt_profile_read(self._h, k, ctypes.byref(ms), ctypes.byref(n),
                                                                 ctypes.byref(b)))

@@ -1,23 +1,33 @@
-// Batched FRSVT of many small independent matrices (
-// PAPER.md P:23 / P:48: WNNM's weighted SVT of many patch-group matrices,
-// per-window problems): ONE CTA per matrix runs the whole of
-// Algorithm 1 in shared memory, so a batch is one launch whose
-// bound is the SM (shared memory and FMA pipes), not HBM.
+// Small FRSVT in one CTA (PAPER.md P:23 / P:48:
+// WNNM's weighted SVT of many patch-group matrices: per-window
+// problems; BASELINE c1: one 200 x 100 fp64 call). ONE CTA per matrix runs the
+// whole of Algorithm 1 with A resident in shared memory, so a
+// call is one launch and a batch is one launch of `batch` CTAs.
 //
-// Per matrix (A m x n fp32, column-major; l <= BT_LMAX; shared Omega n x l):
-//   Y = A Omega                                   (fp32 FMA, Alg. 1 line 3)
+// Per matrix (A m x n, T = fp32 or fp64, column-major; l <= 16 padded with
+// zero columns to LC in {4, 8, 12, 16}; Omega n x l shared by a batch):
+//   Y = A Omega                                   (FMA in T, Alg. 1 line 3)
 //   Q = orth(Y)                                   CGS2 in fp64 with rank reveal
 //   q x { Z = orth(A^T Q); Q = orth(A Z) }        power iteration (lines 13-15)
 //   W = A^T Q  (= B^T)                            (line 16)
-//   one-sided Jacobi on the columns of W:  W V = V_B Sigma, V accumulates U_B
-//                                                 (the SVD of B, lines 16-18; reading Z8)
+//   G = W^T W = B B^T = U_B diag(.) U_B^T         cyclic Jacobi (lines 16-18; reading Z8)
+//   sigma_i = || W u_i ||                         (columns of W U_B = V_B Sigma)
 //   d_i = max(sigma_i - t_i, 0), t_i = tau or w_i (weighted SVT, fn. 1 P:48)
-//   X = (Q V diag(d / sigma)) (W V)^T             Eq. (6)
-// Products of A with the small operands are fp32 sums of at most
-// max(m, n) terms (~1e-6 relative), the orthonormalisation and the Jacobi
-// fp64. Thread block: 256 threads (8 warps).
+//   X = (Q U_B diag(d / sigma)) (W U_B)^T         Eq. (6)
+//
+// Layout: threads own ROWS. Thread t holds rows t, t + 256, ... (RM of them)
+// of the current m x LC (Y, Q) or n x LC (Z, W) block in registers, so the
+// products are row-parallel FMA streams against a broadcast shared-memory
+// row of the small operand, and CGS2 is per-thread partial dot products
+// followed by one block reduction per pass. A sits in shared memory
+// column-major with an odd leading dimension, so both the row-parallel
+// (A X) and the column-parallel (A^T Q) reads are bank-conflict free.
+// The LC x LC eigenproblem runs in one warp, lane k holding row k of G and of
+// U_B in registers; the round-robin pair schedule is unrolled so every
+// register index is static.
 #pragma once
 #include "common.cuh"
+#include "small.cuh"  // philox_normal (the Omega generator)
 
 namespace frsvt {
 
@@ -25,230 +35,655 @@ constexpr int BT_THREADS = 256;
 constexpr int BT_WARPS = BT_THREADS / 32;
 constexpr int BT_LMAX = 16;
 
-__host__ __device__ inline size_t batched_smem_bytes(int m, int n, int l) {
-  // Q (m x l) and W (n x l) fp64, V (l x l) fp64, per-warp scratch, A fp32
-  return ((size_t)(m + n) * l + (size_t)l * l + (size_t)BT_WARPS * BT_LMAX + 4 * BT_LMAX) * sizeof(double) +
-         (size_t)m * n * sizeof(float) + 64;
+// padded width and rows per thread (0: the problem does not fit the design)
+__host__ __device__ inline int bt_lc(int l) { return l <= 4 ? 4 : l <= 8 ? 8 : l <= 12 ? 12 : 16; }
+__host__ __device__ inline int bt_rm(int64_t m, int64_t n) {
+  const int64_t r = m > n ? m : n;
+  return r <= BT_THREADS ? 1 : r <= 4 * BT_THREADS ? 4 : 0;
 }
 
-// Out (rows x l, fp64) = A * In (AX) or A^T * In (ATQ), A in shared memory
-// (m x n fp32, column-major); fp32 accumulation
-__device__ __forceinline__ void bt_ax(const float* __restrict__ sA, int m, int n, int l,
-                                      const double* __restrict__ In, double* __restrict__ Out) {
-  for (int idx = threadIdx.x; idx < m * l; idx += BT_THREADS) {
-    const int i = idx % m, c = idx / m;
-    float acc = 0.f;
-    for (int j = 0; j < n; ++j) acc = fmaf(sA[i + j * m], (float)In[j + c * n], acc);
-    Out[idx] = acc;
+// reduction width: LC rounded up to a power of two
+__host__ __device__ constexpr int bt_kp(int lc) { return lc <= 4 ? 4 : lc <= 8 ? 8 : 16; }
+
+// shared-memory carve-up (bytes, 16-aligned pieces)
+struct BtSmem {
+  int lds, lc;
+  size_t oA, oQ, oW, oGp, oRed, oV, oMisc, total;
+  __host__ __device__ BtSmem(int m, int n, int l, int esz) {
+    lc = bt_lc(l);
+    lds = m | 1;
+    const int kp = bt_kp(lc), ng = lc * (lc + 1) / 2;
+    auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    oA = 0;
+    oQ = al(oA + (size_t)lds * n * esz);                     // m x LC (T), row-major: Q
+    oW = al(oQ + (size_t)m * lc * esz);                      // n x LC (T), row-major: Omega, Z, W U_B
+    oGp = al(oW + (size_t)n * lc * esz);                     // BT_WARPS x LC (LC + 1) / 2 fp64: Gram partials
+    oRed = al(oGp + (size_t)BT_WARPS * ng * 8);              // 2 x (BT_WARPS + 1) x KP fp64: block reductions
+    oV = al(oRed + (size_t)2 * (BT_WARPS + 1) * kp * 8);     // LC x LC fp64 (U_B)
+    oMisc = al(oV + (size_t)lc * lc * 8);                    // sigma, d/sigma (LC each)
+    total = al(oMisc + (size_t)2 * lc * 8);
   }
-}
-__device__ __forceinline__ void bt_atx(const float* __restrict__ sA, int m, int n, int l,
-                                       const double* __restrict__ In, double* __restrict__ Out) {
-  // one warp per output (j, c): lanes split the m rows, shuffle reduction
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int o = warp; o < n * l; o += BT_WARPS) {
-    const int j = o % n, c = o / n;
-    float acc = 0.f;
-    for (int i = lane; i < m; i += 32) acc = fmaf(sA[i + j * m], (float)In[i + c * m], acc);
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (lane == 0) Out[o] = acc;
-  }
+};
+
+__host__ __device__ inline size_t batched_smem_bytes(int m, int n, int l, int esz = 4) {
+  return BtSmem(m, n, l, esz).total;
 }
 
-// CTA sum of one value per thread (fp64); every thread gets the result
-__device__ __forceinline__ double bt_sum(double v, double* scratch) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-  __syncthreads();
-  if (lane == 0) scratch[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < BT_WARPS; ++w) t += scratch[w];
-  return t;
-}
+struct BtArgs {
+  int m, n, l, q;
+  const void* A;
+  int64_t lda, strideA;
+  const void* Om;         // n x l test matrix; nullptr: drawn in the kernel (om_seed, om_stream)
+  int64_t ldo;
+  uint64_t om_seed;
+  uint32_t om_stream;
+  int wmode;
+  double tau;
+  const double* tau_b;    // per-matrix thresholds (wmode 0, nullable)
+  const double* tau_dev;  // one device threshold (wmode 0, nullable)
+  const double* w;        // explicit weights by rank position (wmode 1, device)
+  void* X;
+  int64_t ldx, strideX;
+  int* r_b;               // kept rank
+  double* sig_b;          // sigma by rank position (l per matrix)
+  double* d_b;            // shrunk values by rank position
+  int* s_b;               // revealed rank of the sketch
+  int* sweeps_b;          // Jacobi sweeps
+  double* vs_b;           // residual norm of the last sketch sample (Prop. 4)
+  int* flags;             // FLAG_NONFINITE / FLAG_NOCONV (atomicOr; flags_store: written, batch 1)
+  int flags_store;
+  unsigned long long* stamps;  // test hook: clock64 at phase boundaries (8 per matrix, nullable)
+};
 
-// Orthonormal columns for Y (rows x l, fp64, in place) by classical
-// Gram-Schmidt with one re-orthogonalisation (CGS2); a column whose residual
-// is <= tol of its original norm is numerically dependent and becomes zero
-// (the rank reveal of P:163, reading R4). Returns the kept count.
-__device__ int bt_orth(double* __restrict__ Y, int rows, int l, double tol, double* scratch, double* coef) {
-  int kept = 0;
-  for (int j = 0; j < l; ++j) {
-    double* y = Y + (size_t)j * rows;
-    double loc = 0.0;
-    for (int i = threadIdx.x; i < rows; i += BT_THREADS) loc = fma(y[i], y[i], loc);
-    const double n0 = sqrt(bt_sum(loc, scratch));
-    for (int pass = 0; pass < 2; ++pass) {
-      // coef[k] = Q_k . y for k < j: warp w handles k = w, w + 8, ...
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int k = warp; k < j; k += BT_WARPS) {
-        const double* qk = Y + (size_t)k * rows;
-        double s = 0.0;
-        for (int i = lane; i < rows; i += 32) s = fma(qk[i], y[i], s);
+// Warp-level transposed reduction of KP values (KP a power of two <= 16):
+// at every level each lane keeps half of its values and adds the partner's
+// copy of them (KP - 1 shuffles instead of 5 KP); afterwards v[0] of a lane
+// holds the warp sum of value bt_tr_idx<KP>(lane).
+template <int KP>
+__device__ __forceinline__ int bt_tr_idx(int lane) {
+  int idx = 0, o = 16;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) coef[k] = s;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < rows; i += BT_THREADS) {
-        double v = y[i];
-        for (int k = 0; k < j; ++k) v = fma(-coef[k], Y[i + (size_t)k * rows], v);
-        y[i] = v;
-      }
-      __syncthreads();
+  for (int h = KP / 2; h >= 1; h >>= 1, o >>= 1) idx += (lane & o) ? h : 0;
+  return idx;
+}
+template <int KP>
+__device__ __forceinline__ void bt_warp_tr(double (&v)[KP]) {
+  const int lane = threadIdx.x & 31;
+  int o = 16;
+#pragma unroll
+  for (int h = KP / 2; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? v[k] : v[k + h];
+      const double keep = up ? v[k + h] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
-    loc = 0.0;
-    for (int i = threadIdx.x; i < rows; i += BT_THREADS) loc = fma(y[i], y[i], loc);
-    const double nr = sqrt(bt_sum(loc, scratch));
+  }
+#pragma unroll
+  for (; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+}
+
+// sum over the CTA of v[0..KP) (unused entries zero); every thread gets the
+// sums. Two alternating buffers (BT_WARPS partial rows + the final row), so
+// reductions may follow each other without an extra barrier.
+template <int KP>
+__device__ __forceinline__ void bt_reduce(double (&v)[KP], double* red, int& rb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* part = red + (rb & 1) * (BT_WARPS + 1) * KP;
+  double* fin = part + BT_WARPS * KP;
+  ++rb;
+  bt_warp_tr<KP>(v);
+  if ((lane & (32 / KP - 1)) == 0) part[warp * KP + bt_tr_idx<KP>(lane)] = v[0];
+  __syncthreads();
+  if (warp == 0 && lane < KP) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < BT_WARPS; ++w) s += part[w * KP + lane];
+    fin[lane] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KP; k += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(fin + k);
+    v[k] = t.x;
+    v[k + 1] = t.y;
+  }
+}
+
+// broadcast load of one LC-wide row of a small operand (T, 16-aligned)
+template <typename T, int LC>
+__device__ __forceinline__ void bt_row(const T* __restrict__ p, T (&b)[LC]) {
+  if constexpr (sizeof(T) == 8) {
+#pragma unroll
+    for (int c = 0; c < LC; c += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(p + c);
+      b[c] = v.x;
+      b[c + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < LC; c += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + c);
+      b[c] = v.x;
+      b[c + 1] = v.y;
+      b[c + 2] = v.z;
+      b[c + 3] = v.w;
+    }
+  }
+}
+
+// y (rows tid + 256 r of an m x LC block) = A In, In: n x LC row-major in smem
+template <typename T, int LC, int RM>
+__device__ __forceinline__ void bt_ax(const T* __restrict__ sA, int lds, int m, int n, const T* __restrict__ sIn,
+                                      double (&y)[RM][LC]) {
+  T acc[RM][LC];
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < LC; ++c) acc[r][c] = T(0);
+  const int t = threadIdx.x;
+#pragma unroll 2
+  for (int j = 0; j < n; ++j) {
+    T b[LC];
+    bt_row<T, LC>(sIn + (size_t)j * LC, b);
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      const int i = t + r * BT_THREADS;
+      const T a = i < m ? sA[i + (size_t)j * lds] : T(0);
+#pragma unroll
+      for (int c = 0; c < LC; ++c) acc[r][c] = fma(a, b[c], acc[r][c]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < LC; ++c) y[r][c] = (double)acc[r][c];
+}
+
+// z (rows tid + 256 r of an n x LC block) = A^T In, In: m x LC row-major in smem
+template <typename T, int LC, int RM>
+__device__ __forceinline__ void bt_atx(const T* __restrict__ sA, int lds, int m, int n, const T* __restrict__ sIn,
+                                       double (&z)[RM][LC]) {
+  T acc[RM][LC];
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < LC; ++c) acc[r][c] = T(0);
+  const int t = threadIdx.x;
+#pragma unroll 2
+  for (int i = 0; i < m; ++i) {
+    T b[LC];
+    bt_row<T, LC>(sIn + (size_t)i * LC, b);
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      const int j = t + r * BT_THREADS;
+      const T a = j < n ? sA[i + (size_t)j * lds] : T(0);
+#pragma unroll
+      for (int c = 0; c < LC; ++c) acc[r][c] = fma(a, b[c], acc[r][c]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < LC; ++c) z[r][c] = (double)acc[r][c];
+}
+
+// Orthonormal columns for the register-resident block y (rows x LC) by
+// classical Gram-Schmidt, column by column, re-orthogonalised when needed
+// ("twice is enough": a second pass only when the first removed more than
+// half of the column's squared norm); a column whose residual is <= tol of its
+// original norm is numerically dependent and becomes zero (the rank reveal of
+// P:163, reading R4). Columns >= l are zero padding. Returns the kept count;
+// *last_nr gets the residual norm of column l - 1 (Prop. 4). One block
+// reduction per pass carries (q_k . y for k < j, y . y); the residual norm is
+// ||y||^2 - sum_k c_k^2 (the q_k orthonormal).
+template <int LC, int RM>
+__device__ __forceinline__ int bt_orth(double (&y)[RM][LC], int l, double tol, double* red, int& rb,
+                                       double* last_nr) {
+  constexpr int KP = bt_kp(LC);
+  int kept = 0;
+#pragma unroll
+  for (int j = 0; j < LC; ++j) {
+    if (j >= l) break;
+    double n0sq = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      double v[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        double s = 0.0;
+        if (k <= j) {
+#pragma unroll
+          for (int r = 0; r < RM; ++r) s = fma(y[r][k], y[r][j], s);
+        }
+        v[k] = s;
+      }
+      bt_reduce<KP>(v, red, rb);
+      // y_j -= sum_{k<j} v_k q_k  (v_j is y_j . y_j)
+#pragma unroll
+      for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int k = 0; k < j; ++k) y[r][j] = fma(-v[k], y[r][k], y[r][j]);
+      s2 = v[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s2 = fma(-v[k], v[k], s2);
+      if (pass == 0) n0sq = v[j];
+      if (pass == 0 && s2 > 0.5 * n0sq) break;  // little cancellation: one pass suffices
+    }
+    const double nr = sqrt(fmax(s2, 0.0));
+    const double n0 = sqrt(n0sq);
     const bool keep = n0 > 0.0 && nr > tol * n0;
     const double inv = keep ? 1.0 / nr : 0.0;
-    for (int i = threadIdx.x; i < rows; i += BT_THREADS) y[i] *= inv;
+#pragma unroll
+    for (int r = 0; r < RM; ++r) y[r][j] *= inv;
     kept += keep ? 1 : 0;
-    __syncthreads();
+    if (j == l - 1) *last_nr = nr;
   }
   return kept;
 }
 
-// wmode 0: t_i = tau (scalar, or tau_b[b] when given); 1: t_i = w[i] (host
-// weights copied to the device, length l, shared by the batch)
-__global__ void __launch_bounds__(BT_THREADS)
-batched_frsvt_kernel(int m, int n, int l, int q, const float* __restrict__ Ab, int64_t lda, int64_t strideA,
-                     const float* __restrict__ Om, int64_t ldo, int wmode, double tau,
-                     const double* __restrict__ tau_b, const double* __restrict__ w, float* __restrict__ Xb,
-                     int64_t ldx, int64_t strideX, int* __restrict__ r_b, double* __restrict__ sig_b) {
-  extern __shared__ double bsm[];
-  double* Q = bsm;                               // m x l
-  double* W = Q + (size_t)m * l;                 // n x l: Z, then B^T = A^T Q, then W V
-  double* V = W + (size_t)n * l;                 // l x l
-  double* scratch = V + (size_t)l * l;           // BT_WARPS x BT_LMAX
-  double* coef = scratch + BT_WARPS * BT_LMAX;   // BT_LMAX
-  double* sg = coef + BT_LMAX;                   // sigma (l)
-  double* fd = sg + BT_LMAX;                     // d / sigma (l)
-  float* sA = reinterpret_cast<float*>(fd + 2 * BT_LMAX);
+// store the register block (rows tid + 256 r < rows) to a row-major LC-wide smem array
+template <typename T, int LC, int RM>
+__device__ __forceinline__ void bt_store(const double (&y)[RM][LC], int rows, T* __restrict__ s) {
+#pragma unroll
+  for (int r = 0; r < RM; ++r) {
+    const int i = threadIdx.x + r * BT_THREADS;
+    if (i < rows) {
+#pragma unroll
+      for (int c = 0; c < LC; ++c) s[(size_t)i * LC + c] = (T)y[r][c];
+    }
+  }
+}
+
+// pair (p < q) of round rnd, slot pr of the circle schedule on LC indices
+__host__ __device__ constexpr int bt_pair_a(int LC, int rnd, int pr) { return pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (LC - 1); }
+__host__ __device__ constexpr int bt_pair_b(int LC, int rnd, int pr) { return 1 + (LC - 2 - pr + rnd) % (LC - 1); }
+
+// fast fp64 reciprocal / reciprocal square root: fp32 MUFU seed + two Newton
+// steps (a few ulp); arguments within the fp32 normal range
+__device__ __forceinline__ double bt_rcp(double x) {
+  float f;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)x));
+  double r = f;
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double bt_rsqrt(double x) {
+  double r = rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r;
+}
+
+// Cyclic Jacobi on the symmetric JC x JC matrix held by one warp (lane k <
+// JC: g[] = row k of G, u[] = row k of U, U starting at I; entries >= JC are
+// zero padding). G is first scaled by 1 / trace (eigenvectors unchanged;
+// every quantity then stays in the fp32 range the fast reciprocals need).
+// Round-robin (circle) pair schedule, the JC/2 rotations of a round applied
+// together: G <- J^T G J, U <- U J. Lane p of pair (p, q) computes its
+// rotation, the other lanes get it by shuffles; the rotated off-diagonal
+// entry is then set to exactly 0. A pair rotates while
+// g_pq^2 > tol^2 |g_pp g_qq| and |g_pq| > 1e-17 (trace 1; below that lies
+// the Gram's own rounding). Returns the sweeps; *conv: a sweep without a
+// rotation was reached.
+template <int JC, int LC>
+__device__ __forceinline__ int bt_jacobi(double (&g)[LC], double (&u)[LC], double tol, bool* conv) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double tr = 0.0;
+#pragma unroll
+  for (int k = 0; k < JC; ++k) tr += __shfl_sync(full, g[k], k);
+  const double sc = tr > 0.0 ? 1.0 / tr : 1.0;
+#pragma unroll
+  for (int k = 0; k < JC; ++k) g[k] *= sc;
+  const double fl = 1e-17, tol2 = tol * tol;
+  int sweep = 0;
+  *conv = false;
+  for (; sweep < 30; ++sweep) {
+    bool anyl = false;
+#pragma unroll
+    for (int rnd = 0; rnd < JC - 1; ++rnd) {
+      // this lane's partner and role (static register indices only)
+      int partner = lane;
+      bool isp = true;
+      double dg = 0.0, off = 0.0;
+#pragma unroll
+      for (int pr = 0; pr < JC / 2; ++pr) {
+        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
+        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
+        if (lane == p) { partner = q; isp = true; dg = g[p]; off = g[q]; }
+        if (lane == q) { partner = p; isp = false; dg = g[q]; off = g[p]; }
+      }
+      const double dq = __shfl_sync(full, dg, partner);
+      double c = 1.0, s = 0.0;
+      bool rot = false;
+      if (isp && lane < JC && off * off > tol2 * fabs(dg * dq) && fabs(off) > fl) {
+        // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
+        // zeta = (g_qq - g_pp) / (2 g_pq): t = sgn(zeta) 2|g_pq| / (|dif| + sqrt(dif^2 + 4 g_pq^2))
+        const double dif = dq - dg;
+        const double sg = ((dif >= 0.0) == (off >= 0.0)) ? 1.0 : -1.0;
+        const double h2 = fma(dif, dif, 4.0 * off * off);
+        const double den = fabs(dif) + h2 * bt_rsqrt(h2);
+        const double t = sg * 2.0 * fabs(off) * bt_rcp(den);
+        c = bt_rsqrt(fma(t, t, 1.0));
+        s = c * t;
+        rot = true;
+      }
+      anyl |= rot;
+      {
+        const double cq = __shfl_sync(full, c, partner), sq = __shfl_sync(full, s, partner);
+        const bool rq = __shfl_sync(full, rot ? 1 : 0, partner) != 0;
+        if (!isp) { c = cq; s = sq; rot = rq; }
+      }
+      // columns: G <- G J, U <- U J (every lane its own row; pair (p, q) uses lane p's c, s)
+#pragma unroll
+      for (int pr = 0; pr < JC / 2; ++pr) {
+        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
+        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
+        const double cc = __shfl_sync(full, c, p), ss = __shfl_sync(full, s, p);
+        const double gp = g[p], gq = g[q];
+        g[p] = cc * gp - ss * gq;
+        g[q] = ss * gp + cc * gq;
+        const double up = u[p], uq = u[q];
+        u[p] = cc * up - ss * uq;
+        u[q] = ss * up + cc * uq;
+      }
+      // rows: G <- J^T G (rows p and q of a pair exchange through shuffles)
+#pragma unroll
+      for (int k = 0; k < JC; ++k) {
+        const double o = __shfl_sync(full, g[k], partner);
+        g[k] = isp ? (c * g[k] - s * o) : (s * o + c * g[k]);
+      }
+      // the rotated pair's off-diagonal is zero by construction
+#pragma unroll
+      for (int pr = 0; pr < JC / 2; ++pr) {
+        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
+        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
+        if (rot && lane == p) g[q] = 0.0;
+        if (rot && lane == q) g[p] = 0.0;
+      }
+    }
+    if (!__any_sync(full, anyl)) {
+      ++sweep;
+      *conv = true;
+      break;
+    }
+  }
+  return sweep;
+}
+
+template <typename T, int LC, int RM>
+__global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) {
+  extern __shared__ __align__(16) unsigned char bsm_raw[];
+  const int m = a.m, n = a.n, l = a.l;
+  const BtSmem L(m, n, l, (int)sizeof(T));
+  T* sA = reinterpret_cast<T*>(bsm_raw + L.oA);
+  T* sQ = reinterpret_cast<T*>(bsm_raw + L.oQ);
+  T* sW = reinterpret_cast<T*>(bsm_raw + L.oW);
+  double* sGp = reinterpret_cast<double*>(bsm_raw + L.oGp);
+  double* red = reinterpret_cast<double*>(bsm_raw + L.oRed);
+  double* sV = reinterpret_cast<double*>(bsm_raw + L.oV);
+  double* sg = reinterpret_cast<double*>(bsm_raw + L.oMisc);
+  double* fd = sg + LC;
+  const int lds = L.lds;
   const int b = blockIdx.x;
-  const float* A = Ab + (int64_t)b * strideA;
-  const int tid = threadIdx.x;
-  const double tol = 1e-6;  // fp32 data: a sample whose residual is below 1e-6 of its norm carries no direction
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned long long* stamp = a.stamps ? a.stamps + (size_t)b * 8 : nullptr;
+  if (stamp && tid == 0) stamp[0] = clock64();
+  const T* A = reinterpret_cast<const T*>(a.A) + (int64_t)b * a.strideA;
+  const T* Om = reinterpret_cast<const T*>(a.Om);
+  // a sample whose residual is below this fraction of its norm carries no
+  // direction (fp32 data 1e-6, fp64 data 1e-13; reading R4)
+  const double tol = sizeof(T) == 4 ? 1e-6 : 1e-13;
+  // A into shared memory with asynchronous copies (every element in flight at once)
   for (int idx = tid; idx < m * n; idx += BT_THREADS) {
     const int i = idx % m, j = idx / m;
-    sA[idx] = A[i + (int64_t)j * lda];
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(sA + i + (size_t)j * lds);
+    const T* src = A + i + (int64_t)j * a.lda;
+    if constexpr (sizeof(T) == 8)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
   }
-  // Omega (n x l) into W as fp64, then Y = A Omega into Q
-  for (int idx = tid; idx < n * l; idx += BT_THREADS) W[idx] = Om[idx % n + (int64_t)(idx / n) * ldo];
-  __syncthreads();
-  bt_ax(sA, m, n, l, W, Q);
-  __syncthreads();
-  bt_orth(Q, m, l, tol, scratch, coef);
-  for (int it = 0; it < q; ++it) {
-    bt_atx(sA, m, n, l, Q, W);
-    __syncthreads();
-    bt_orth(W, n, l, tol, scratch, coef);
-    bt_ax(sA, m, n, l, W, Q);
-    __syncthreads();
-    bt_orth(Q, m, l, tol, scratch, coef);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // Omega (n x l) into sW row-major, zero padded to LC columns (drawn here
+  // while A is in flight when no explicit Omega is given: element (j, c) is
+  // normal number c n + j of the Philox stream, as omega_kernel)
+  for (int idx = tid; idx < n * LC; idx += BT_THREADS) {
+    const int j = idx / LC, c = idx % LC;
+    T v = T(0);
+    if (c < l) v = Om ? Om[j + (int64_t)c * a.ldo] : (T)philox_normal(a.om_seed, a.om_stream, (uint64_t)c * n + j);
+    sW[idx] = v;
   }
-  bt_atx(sA, m, n, l, Q, W);  // W = B^T
-  for (int idx = tid; idx < l * l; idx += BT_THREADS) V[idx] = (idx % l == idx / l) ? 1.0 : 0.0;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  // one-sided Jacobi on the columns of W (n x l): round-robin pairs, warp w
-  // takes pair w of the round; V accumulates the rotations (U_B)
-  const int warp = tid >> 5, lane = tid & 31;
-  const int L2 = (l + 1) & ~1;
-  for (int sweep = 0; sweep < 30; ++sweep) {
-    int rotated = 0;
-    for (int rnd = 0; rnd < L2 - 1; ++rnd) {
-      for (int pr = warp; pr < L2 / 2; pr += BT_WARPS) {
-        // circle ordering: position 0 fixed, the others rotate by rnd
-        const int a0 = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (L2 - 1);
-        const int b0 = 1 + (L2 - 2 - pr + rnd) % (L2 - 1);
-        const int pcol = min(a0, b0), qcol = max(a0, b0);
-        if (qcol >= l) continue;
-        double* wp = W + (size_t)pcol * n;
-        double* wq = W + (size_t)qcol * n;
-        double al = 0.0, be = 0.0, g = 0.0;
-        for (int i = lane; i < n; i += 32) {
-          al = fma(wp[i], wp[i], al);
-          be = fma(wq[i], wq[i], be);
-          g = fma(wp[i], wq[i], g);
-        }
+  if (stamp && tid == 0) stamp[1] = clock64();
+  int rb = 0;
+  double vs_raw = 0.0, dummy = 0.0;
+  double y[RM][LC];
+  bt_ax<T, LC, RM>(sA, lds, m, n, sW, y);
+  int s_kept = bt_orth<LC, RM>(y, l, tol, red, rb, &vs_raw);
+  bt_store<T, LC, RM>(y, m, sQ);
+  __syncthreads();
+  if (stamp && tid == 0) stamp[2] = clock64();
+  for (int it = 0; it < a.q; ++it) {
+    bt_atx<T, LC, RM>(sA, lds, m, n, sQ, y);
+    bt_orth<LC, RM>(y, l, tol, red, rb, &dummy);
+    bt_store<T, LC, RM>(y, n, sW);
+    __syncthreads();
+    bt_ax<T, LC, RM>(sA, lds, m, n, sW, y);
+    s_kept = bt_orth<LC, RM>(y, l, tol, red, rb, &dummy);
+    bt_store<T, LC, RM>(y, m, sQ);
+    __syncthreads();
+  }
+  if (stamp && tid == 0) stamp[3] = clock64();
+  // W = A^T Q (= B^T) in registers; per-warp partials of G = W^T W (upper
+  // triangle, row-major packed, entry e(p, q) = p LC - p (p - 1) / 2 + q - p),
+  // 16 entries per transposed warp reduction
+  bt_atx<T, LC, RM>(sA, lds, m, n, sQ, y);
+  constexpr int NG = LC * (LC + 1) / 2;
+  {
+    double* gp = sGp + (size_t)warp * NG;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          g += __shfl_xor_sync(0xffffffffu, g, o);
-        }
-        if (g != 0.0 && fabs(g) > 1e-15 * sqrt(al * be)) {
-          rotated = 1;
-          const double zeta = (be - al) / (2.0 * g);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = lane; i < n; i += 32) {
-            const double x = wp[i], y = wq[i];
-            wp[i] = c * x - s * y;
-            wq[i] = s * x + c * y;
-          }
-          for (int i = lane; i < l; i += 32) {
-            const double x = V[i + pcol * l], y = V[i + qcol * l];
-            V[i + pcol * l] = c * x - s * y;
-            V[i + qcol * l] = s * x + c * y;
+    for (int c0 = 0; c0 < NG; c0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = 0.0;
+      int e = 0;
+#pragma unroll
+      for (int p = 0; p < LC; ++p) {
+#pragma unroll
+        for (int q2 = p; q2 < LC; ++q2, ++e) {
+          if (e >= c0 && e < c0 + 16) {
+            double s = 0.0;
+#pragma unroll
+            for (int r = 0; r < RM; ++r) s = fma(y[r][p], y[r][q2], s);
+            v[e - c0] = s;
           }
         }
       }
-      __syncthreads();
+      bt_warp_tr<16>(v);
+      const int eo = c0 + bt_tr_idx<16>(lane);
+      if ((lane & 1) == 0 && eo < NG) gp[eo] = v[0];
     }
-    if (!__syncthreads_or(rotated)) break;
-  }
-  // sigma_i = |W_i|, shrink
-  for (int i = warp; i < l; i += BT_WARPS) {
-    double s2 = 0.0;
-    for (int k = lane; k < n; k += 32) s2 = fma(W[k + i * n], W[k + i * n], s2);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (lane == 0) sg[i] = sqrt(s2);
   }
   __syncthreads();
-  if (tid == 0) {
-    // thresholds on sigma sorted descending (rank positions)
-    int r = 0;
-    for (int i = 0; i < l; ++i) {
+  if (stamp && tid == 0) stamp[4] = clock64();
+  int sweeps = 0;
+  bool conv = true;
+  if (warp == 0) {
+    double g[LC], u[LC];
+    const int k = lane < LC ? lane : 0;
+#pragma unroll
+    for (int c = 0; c < LC; ++c) {
+      const int p = k < c ? k : c, q2 = k < c ? c : k;
+      const int e = p * LC - p * (p - 1) / 2 + q2 - p;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < BT_WARPS; ++w) s += sGp[(size_t)w * NG + e];
+      g[c] = s;
+      u[c] = c == k ? 1.0 : 0.0;
+    }
+    const double jtol = sizeof(T) == 8 ? 1e-15 : 1e-9;
+    // the rounds run over l rounded up to even (JC = LC - 2 when that covers l)
+    if constexpr (LC > 4) {
+      if (l <= LC - 2) sweeps = bt_jacobi<LC - 2, LC>(g, u, jtol, &conv);
+      else sweeps = bt_jacobi<LC, LC>(g, u, jtol, &conv);
+    } else {
+      if (l <= 2) sweeps = bt_jacobi<2, LC>(g, u, jtol, &conv);
+      else sweeps = bt_jacobi<LC, LC>(g, u, jtol, &conv);
+    }
+    if (lane < LC) {
+#pragma unroll
+      for (int c = 0; c < LC; ++c) sV[lane * LC + c] = u[c];
+    }
+  }
+  __syncthreads();
+  if (stamp && tid == 0) stamp[5] = clock64();
+  // W U_B in place (rows in registers), sigma_c = || (W U_B)_c ||
+#pragma unroll
+  for (int r = 0; r < RM; ++r) {
+    double t[LC];
+#pragma unroll
+    for (int c = 0; c < LC; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LC; ++k) s = fma(y[r][k], sV[k * LC + c], s);
+      t[c] = s;
+    }
+#pragma unroll
+    for (int c = 0; c < LC; ++c) y[r][c] = t[c];
+  }
+  {
+    constexpr int KP = bt_kp(LC);
+    double v[KP];
+#pragma unroll
+    for (int c = 0; c < KP; ++c) {
+      double s = 0.0;
+      if (c < LC) {
+#pragma unroll
+        for (int r = 0; r < RM; ++r) s = fma(y[r][c], y[r][c], s);
+      }
+      v[c] = s;
+    }
+    bt_reduce<KP>(v, red, rb);
+#pragma unroll
+    for (int c = 0; c < LC; ++c)
+      if (tid == c) sg[c] = sqrt(v[c]);
+  }
+  bt_store<T, LC, RM>(y, n, sW);
+  __syncthreads();
+  if (warp == 0) {
+    // thresholds on sigma sorted descending (rank positions; padding sorts
+    // last); lane i handles sigma_i
+    const int i = lane;
+    bool bad = false, pos_ok = false;
+    double d = 0.0;
+    if (i < LC) {
+      const double si = sg[i];
+      bad = !isfinite(si);
       int pos = 0;
-      for (int k = 0; k < l; ++k) pos += (sg[k] > sg[i]) || (sg[k] == sg[i] && k < i);
-      const double t = wmode == 1 ? w[pos] : (tau_b ? tau_b[b] : tau);
-      const double d = fmax(sg[i] - t, 0.0);
-      fd[i] = (d > 0.0 && sg[i] > 0.0) ? d / sg[i] : 0.0;
-      r += d > 0.0;
-      if (sig_b) sig_b[(int64_t)b * l + pos] = sg[i];
+#pragma unroll
+      for (int k = 0; k < LC; ++k) {
+        const double sk = sg[k];
+        pos += (sk > si) || (sk == si && k < i);
+      }
+      pos_ok = pos < l;
+      double t;
+      if (a.wmode == 1) t = pos_ok ? a.w[pos] : 0.0;
+      else t = a.tau_b ? a.tau_b[b] : (a.tau_dev ? *a.tau_dev : a.tau);
+      d = pos_ok ? fmax(si - t, 0.0) : 0.0;
+      fd[i] = (d > 0.0 && si > 0.0) ? d / si : 0.0;
+      if (pos_ok) {
+        if (a.sig_b) a.sig_b[(int64_t)b * l + pos] = si;
+        if (a.d_b) a.d_b[(int64_t)b * l + pos] = d;
+      }
     }
-    if (r_b) r_b[b] = r;
+    const int r = __popc(__ballot_sync(0xffffffffu, d > 0.0));
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (a.r_b) a.r_b[b] = r;
+      if (a.s_b) a.s_b[b] = s_kept;
+      if (a.vs_b) a.vs_b[b] = vs_raw;
+      if (a.sweeps_b) a.sweeps_b[b] = sweeps;
+      const int fl = (anybad ? FLAG_NONFINITE : 0) | (conv ? 0 : FLAG_NOCONV);
+      if (a.flags && a.flags_store) *a.flags = fl;
+      else if (a.flags && fl) atomicOr(a.flags, fl);
+    }
   }
   __syncthreads();
-  // P = Q V diag(d / sigma) into Q's place (row by row: each thread owns rows)
-  for (int i = tid; i < m; i += BT_THREADS) {
-    double row[BT_LMAX];
+  if (stamp && tid == 0) stamp[6] = clock64();
+  // X = P (W U_B)^T, P = Q U_B diag(d / sigma); thread = row i of X (coalesced stores)
+  T* X = reinterpret_cast<T*>(a.X) + (int64_t)b * a.strideX;
 #pragma unroll
-    for (int c = 0; c < BT_LMAX; ++c) row[c] = 0.0;
-    for (int k = 0; k < l; ++k) {
-      const double qk = Q[i + (size_t)k * m];
+  for (int r = 0; r < RM; ++r) {
+    const int i = tid + r * BT_THREADS;
+    if (i >= m) continue;
+    T qrow[LC];
+    bt_row<T, LC>(sQ + (size_t)i * LC, qrow);
+    T pr[LC];
 #pragma unroll
-      for (int c = 0; c < BT_LMAX; ++c)
-        if (c < l) row[c] = fma(qk, V[k + c * l], row[c]);
+    for (int c = 0; c < LC; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < LC; ++k) s = fma((double)qrow[k], sV[k * LC + c], s);
+      pr[c] = (T)(s * fd[c]);
     }
+#pragma unroll 2
+    for (int j = 0; j < n; ++j) {
+      T wr[LC];
+      bt_row<T, LC>(sW + (size_t)j * LC, wr);
+      T acc = T(0);
 #pragma unroll
-    for (int c = 0; c < BT_LMAX; ++c)
-      if (c < l) Q[i + (size_t)c * m] = row[c] * fd[c];
+      for (int c = 0; c < LC; ++c) acc = fma(pr[c], wr[c], acc);
+      X[i + (int64_t)j * a.ldx] = acc;
+    }
   }
-  __syncthreads();
-  // X = P W^T (W = B^T V = V_B Sigma)
-  float* X = Xb + (int64_t)b * strideX;
-  for (int idx = tid; idx < m * n; idx += BT_THREADS) {
-    const int i = idx % m, j = idx / m;
-    double acc = 0.0;
-    for (int c = 0; c < l; ++c) acc = fma(Q[i + (size_t)c * m], W[j + (size_t)c * n], acc);
-    X[i + (int64_t)j * ldx] = (float)acc;
+  if (stamp) {
+    __syncthreads();
+    if (tid == 0) stamp[7] = clock64();
   }
+}
+
+// eligibility of a problem for the one-CTA design
+__host__ inline bool bt_fits(int64_t m, int64_t n, int l, int esz) {
+  return l >= 1 && l <= BT_LMAX && m >= 1 && n >= 1 && bt_rm(m, n) != 0 &&
+         batched_smem_bytes((int)m, (int)n, l, esz) <= 227 * 1024;
+}
+
+template <typename T, int LC, int RM>
+__host__ inline cudaError_t bt_launch_t(const BtArgs& a, int batch, cudaStream_t st) {
+  const size_t smem = batched_smem_bytes(a.m, a.n, a.l, (int)sizeof(T));
+  batched_frsvt_kernel<T, LC, RM><<<(unsigned)batch, BT_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// launch (the caller checked bt_fits and set the shared-memory attributes)
+template <typename T>
+__host__ inline cudaError_t bt_launch(const BtArgs& a, int batch, cudaStream_t st) {
+  const int lc = bt_lc(a.l);
+  const int rm = bt_rm(a.m, a.n);
+#define BT_CASE(LCV, RMV) \
+  if (lc == LCV && rm == RMV) return bt_launch_t<T, LCV, RMV>(a, batch, st);
+  BT_CASE(4, 1) BT_CASE(8, 1) BT_CASE(12, 1) BT_CASE(16, 1)
+  BT_CASE(4, 4) BT_CASE(8, 4) BT_CASE(12, 4) BT_CASE(16, 4)
+#undef BT_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+__host__ inline cudaError_t bt_set_attrs() {
+  const int mx = 227 * 1024;
+  cudaError_t e = cudaSuccess;
+#define BT_ATTR(LCV, RMV) \
+  if (e == cudaSuccess)   \
+    e = cudaFuncSetAttribute(batched_frsvt_kernel<T, LCV, RMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  BT_ATTR(4, 1) BT_ATTR(8, 1) BT_ATTR(12, 1) BT_ATTR(16, 1)
+  BT_ATTR(4, 4) BT_ATTR(8, 4) BT_ATTR(12, 4) BT_ATTR(16, 4)
+#undef BT_ATTR
+  return e;
 }
 
 }  // namespace frsvt

@@ -121,6 +121,7 @@ struct frsvt_handle {
   int use_tc;        // fp32 handle with TMA available: tcgen05 passes (else SIMT, fp64 handles)
   int tc_m;          // tensor-core small-operand path for the m-row matrices (Y, Q); rank-uniform
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
+  int single_cta;    // the last frsvt_apply ran on the single-CTA path (FRSVT_FLAG_SINGLE_CTA)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_OPT_FUSED_SKETCH)
   int ap_on, ap_a, ap_jump, ap_b, ap_l0;  // adaptive rank prediction (Eq. 7), frsvt_set_adaptive_rank
   int keep;          // partial SVT of the current rpca step (rpca_state.keep; 0 for frsvt_apply*)
@@ -162,8 +163,8 @@ struct frsvt_handle {
   std::vector<cudaEvent_t>* prof_ev;   // pool, pairs (start, end)
   std::vector<int>* prof_kind;         // kind per used pair
   size_t prof_used;
-  double prof_ms[3], prof_bytes[3];
-  int64_t prof_count[3];
+  double prof_ms[4], prof_bytes[4];
+  int64_t prof_count[4];
 };
 
 #define CK(x)                                                                      \
@@ -1099,7 +1100,7 @@ frsvt_status fill_info(frsvt_handle* h, frsvt_info* info) {
   memset(info, 0, sizeof(*info));
   info->s = ds.s;
   info->r = ds.r;
-  info->flags = ds.flags;
+  info->flags = ds.flags | (h->single_cta ? FRSVT_FLAG_SINGLE_CTA : 0);
   info->sweeps = ds.sweeps;
   info->calls = h->call;
   info->mu = ds.mu[0];
@@ -1113,6 +1114,56 @@ frsvt_status fill_info(frsvt_handle* h, frsvt_info* info) {
   return FRSVT_OK;
 }
 
+// A call small enough for one SM (BASELINE c1: 200 x 100, l = 10) runs all of
+// Algorithm 1 in one CTA's shared memory (batched.cuh with batch 1): no range
+// propagation, one rank, plain or explicit-weight thresholds, l <= 16.
+template <typename T>
+bool single_cta_ok(const frsvt_handle* h, int wmode) {
+  return !h->rp && h->cfg.nranks == 1 && h->group == nullptr && !h->ap_on && h->keep == 0 &&
+         (wmode == 0 || wmode == 1) && bt_fits(h->m, h->n, h->l, (int)sizeof(T));
+}
+
+template <typename T>
+frsvt_status single_cta_apply(frsvt_handle* h, const T* A, int64_t lda, int wmode, double tau, T* X,
+                              int64_t ldx) {
+  NvtxRange nv("frsvt.single_cta");
+  // Omega: the override, else drawn inside the kernel (same generator and
+  // stream as omega_kernel)
+  const T* ov = h->override_pending ? (const T*)h->OmOv : nullptr;
+  h->override_pending = 0;
+  DevState* d = h->dev;
+  BtArgs a{};
+  a.m = (int)h->m;
+  a.n = (int)h->n;
+  a.l = h->l;
+  a.q = h->q;
+  a.A = A;
+  a.lda = lda;
+  a.Om = ov;
+  a.ldo = h->n;
+  a.om_seed = h->cfg.seed;
+  a.om_stream = 1000u + (uint32_t)h->call;
+  a.wmode = wmode;
+  a.tau = tau;
+  a.w = h->wvec;
+  a.X = X;
+  a.ldx = ldx;
+  a.r_b = &d->r;
+  a.sig_b = d->rep;
+  a.d_b = d->rep + FRSVT_LMAX;
+  a.s_b = &d->s;
+  a.sweeps_b = &d->sweeps;
+  a.vs_b = &d->varsig_raw;
+  a.flags = &d->flags;
+  a.flags_store = 1;
+  TRY(prof_begin(h));
+  CK(bt_launch<T>(a, 1, h->st));
+  TRY(post_launch(h));
+  TRY(prof_end(h, 3, 2.0 * (double)h->m * h->n * h->l * (2 * h->q + 3)));
+  h->call++;
+  return FRSVT_OK;
+}
+
 template <typename T>
 frsvt_status apply_impl(frsvt_handle* h, const void* A, int64_t lda, int wmode, double tau,
                         const double* w_host, double C, double eps, void* X, int64_t ldx,
@@ -1122,7 +1173,13 @@ frsvt_status apply_impl(frsvt_handle* h, const void* A, int64_t lda, int wmode, 
     tau = w_host[0];  // smallest explicit threshold (the small SVD's exact early-out)
     for (int i = 1; i < h->l; ++i) tau = fmin(tau, w_host[i]);
   }
-  CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  h->keep = 0;  // partial SVT (keep) belongs to rpca_state only
+  h->single_cta = single_cta_ok<T>(h, wmode) ? 1 : 0;
+  if (!h->single_cta) CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
+  if (h->single_cta) {
+    TRY(single_cta_apply<T>(h, (const T*)A, lda, wmode, tau, (T*)X, ldx));
+    return fill_info(h, info);
+  }
   TRY(frsvt_core<T>(h, (const T*)A, lda, wmode, tau, nullptr, C, eps));
   TRY(compose_X<T>(h, (T*)X, ldx));
   return fill_info(h, info);
@@ -1150,6 +1207,7 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
   T* A = (T*)st->A;
   CK(cudaMemsetAsync(&h->dev->flags, 0, sizeof(int), h->st));
   h->keep = st->keep;
+  h->single_cta = 0;
   if (st->iter == 0) {
     // ---- init: norms, mu_0, Y_0, E_1, A_1 ----
     const int nb = grid1d(h->m * h->n);
@@ -1241,6 +1299,8 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR(lowdin_series_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(eig_jacobi_kernel, EigJacobi::smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(chol_inv_kernel<float>, chol_inv_smem_bytes());
+  CK(bt_set_attrs<float>());  // single-CTA path and frsvt_batched_apply
+  CK(bt_set_attrs<double>());
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 32>), tc::PassSmem::total(32));
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 64>), tc::PassSmem::total(64));
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 128>), tc::PassSmem::total(128));
@@ -1310,14 +1370,29 @@ frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l,
   } else {
     return FRSVT_EINVAL;
   }
-  const size_t smem = batched_smem_bytes((int)m, (int)n, l);
-  if (smem > 227 * 1024 || m > (1 << 20) || n > (1 << 20)) return FRSVT_EINVAL;
+  if (!bt_fits(m, n, l, 4)) return FRSVT_EINVAL;
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  CK(cudaFuncSetAttribute(batched_frsvt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  batched_frsvt_kernel<<<(unsigned)batch, BT_THREADS, smem, st>>>((int)m, (int)n, l, q, A, lda, strideA, Omega, ldo,
-                                                                    wmode, tau, tau_batch, w, X, ldx, strideX, r_out,
-                                                                    sigma_out);
-  CK(cudaGetLastError());
+  CK(bt_set_attrs<float>());
+  BtArgs a{};
+  a.m = (int)m;
+  a.n = (int)n;
+  a.l = l;
+  a.q = q;
+  a.A = A;
+  a.lda = lda;
+  a.strideA = strideA;
+  a.Om = Omega;
+  a.ldo = ldo;
+  a.wmode = wmode;
+  a.tau = tau;
+  a.tau_b = tau_batch;
+  a.w = w;
+  a.X = X;
+  a.ldx = ldx;
+  a.strideX = strideX;
+  a.r_b = r_out;
+  a.sig_b = sigma_out;
+  CK(bt_launch<float>(a, batch, st));
   return FRSVT_OK;
 }
 
@@ -1824,7 +1899,7 @@ frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable) {
   if (!h) return FRSVT_EINVAL;
   CK(cudaStreamSynchronize(h->st));
   h->prof_used = 0;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     h->prof_ms[k] = 0.0;
     h->prof_bytes[k] = 0.0;
     h->prof_count[k] = 0;
@@ -1834,7 +1909,7 @@ frsvt_status frsvt_profile(frsvt_handle* h, int32_t enable) {
 }
 
 frsvt_status frsvt_profile_read(frsvt_handle* h, int32_t kind, double* ms, int64_t* launches, double* bytes) {
-  if (!h || kind < 0 || kind > 2) return FRSVT_EINVAL;
+  if (!h || kind < 0 || kind > 3) return FRSVT_EINVAL;
   TRY(prof_flush(h));
   if (ms) *ms = h->prof_ms[kind];
   if (launches) *launches = h->prof_count[kind];

@@ -172,6 +172,42 @@ def test_edge_cases(P, dtype):
     assert z14(Bc, Xe, B64) <= (1e-4 if dtype == torch.float32 else 1e-10)
 
 
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.float64, 1e-10)])
+@pytest.mark.parametrize("m,n,l,q,rank", [(200, 100, 10, 1, 5), (64, 300, 16, 2, 9), (500, 40, 5, 0, 3),
+                                          (33, 17, 1, 1, 1), (150, 100, 16, 3, 12)])
+def test_single_cta_path(P, m, n, l, q, rank, dtype, tol):
+    """Calls small enough for one SM (no RP, l <= 16) run Algorithm 1 in one
+    CTA (batched.cuh): scalar and explicit-weight thresholds against the
+    oracle, the flag reports the path, and an RP handle of the same shape
+    keeps the multi-kernel path."""
+    A = _lowrank_plus_noise(m, n, rank, 1e-2, seed=m * n + l)
+    Ag = cm(A, dtype)
+    A64 = np64(Ag)
+    sA = np.linalg.svd(A64, compute_uv=False)
+    tau = 0.5 * (sA[rank - 1] + sA[rank]) if rank < min(m, n) else 0.5 * sA[-1]
+    seed = 4242 + l
+    Om = omega(seed, 0, n, l).numpy()
+    ref = oracle.frsvt(A64, Om, l, q, tau=tau, rp=False)
+    h = P.Frsvt(m, n, l, q, rp=False, dtype=dtype, seed=seed)
+    X, info = h.apply(Ag, tau, info=True)
+    assert info.flags & P.FLAG_SINGLE_CTA
+    assert z14(X, ref.X, A64) <= tol
+    assert info.r == ref.r and info.s == ref.s
+    assert np.allclose(np.array(info.sigma[: ref.s]), ref.sigma, rtol=1e-5 if dtype == torch.float32 else 1e-12)
+    # explicit weights: the first two untouched, the rest at tau
+    w = np.concatenate([np.zeros(min(2, l)), np.full(l - min(2, l), tau)])
+    Om1 = omega(seed, 1, n, l).numpy()
+    refw = oracle.frsvt(A64, Om1, l, q, w=w, rp=False)
+    Xw, infow = h.apply_weighted(Ag, P.W_EXPLICIT, w=w, info=True)
+    assert infow.flags & P.FLAG_SINGLE_CTA
+    assert z14(Xw, refw.X, A64) <= tol
+    # the same shape with range propagation takes the multi-kernel path
+    hr = P.Frsvt(m, n, l, q, rp=True, dtype=dtype, seed=seed)
+    Xr, infor = hr.apply(Ag, tau, info=True)
+    assert not infor.flags & P.FLAG_SINGLE_CTA
+    assert z14(Xr, ref.X, A64) <= tol
+
+
 def test_nonfinite_is_reported(P):
     h = P.Frsvt(64, 40, 6, 1, rp=False, dtype=torch.float32, seed=1)
     A = torch.randn(40, 64, device="cuda").t()
