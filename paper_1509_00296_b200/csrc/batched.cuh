@@ -92,7 +92,7 @@ struct BtArgs {
   double* vs_b;           // residual norm of the last sketch sample (Prop. 4)
   int* flags;             // FLAG_NONFINITE / FLAG_NOCONV (atomicOr; flags_store: written, batch 1)
   int flags_store;
-  unsigned long long* stamps;  // test hook: clock64 at phase boundaries (8 per matrix, nullable)
+  int stop_after;         // test hook (phase timing): 0 = run everything, k = return after phase k (1..6)
 };
 
 // Warp-level transposed reduction of KP values (KP a power of two <= 16):
@@ -296,40 +296,43 @@ __device__ __forceinline__ void bt_store(const double (&y)[RM][LC], int rows, T*
   }
 }
 
-// pair (p < q) of round rnd, slot pr of the circle schedule on LC indices
-__host__ __device__ constexpr int bt_pair_a(int LC, int rnd, int pr) { return pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (LC - 1); }
-__host__ __device__ constexpr int bt_pair_b(int LC, int rnd, int pr) { return 1 + (LC - 2 - pr + rnd) % (LC - 1); }
-
-// fast fp64 reciprocal / reciprocal square root: fp32 MUFU seed + two Newton
-// steps (a few ulp); arguments within the fp32 normal range
-__device__ __forceinline__ double bt_rcp(double x) {
-  float f;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"((float)x));
-  double r = f;
-  r = r * fma(-x, r, 2.0);
-  r = r * fma(-x, r, 2.0);
-  return r;
+// Circle-method ring on JC slots (pair q = slots (2q, 2q + 1)): slot 0 stays,
+// the others advance T[1] -> T[2] -> ... -> T[h-1] -> B[h-1] -> ... -> B[0] ->
+// T[1] (T[q] = slot 2q, B[q] = slot 2q + 1). After JC - 1 rounds every pair
+// of columns has met once and the ring is back at its start.
+template <int JC, int LC, typename V>
+__device__ __forceinline__ void bt_ring(V (&a)[LC]) {
+  if constexpr (JC > 2) {
+    constexpr int h = JC / 2;
+    V o[JC];
+#pragma unroll
+    for (int k = 0; k < JC; ++k) o[k] = a[k];
+#pragma unroll
+    for (int q = 1; q < h - 1; ++q) a[2 * (q + 1)] = o[2 * q];
+    a[2 * (h - 1) + 1] = o[2 * (h - 1)];
+#pragma unroll
+    for (int q = 0; q < h - 1; ++q) a[2 * q + 1] = o[2 * (q + 1) + 1];
+    a[2] = o[1];
+  }
 }
-__device__ __forceinline__ double bt_rsqrt(double x) {
-  double r = rsqrtf((float)x);
-  r = r * fma(-0.5 * x * r, r, 1.5);
-  r = r * fma(-0.5 * x * r, r, 1.5);
-  return r;
-}
 
-// Cyclic Jacobi on the symmetric JC x JC matrix held by one warp (lane k <
-// JC: g[] = row k of G, u[] = row k of U, U starting at I; entries >= JC are
-// zero padding). G is first scaled by 1 / trace (eigenvectors unchanged;
-// every quantity then stays in the fp32 range the fast reciprocals need).
-// Round-robin (circle) pair schedule, the JC/2 rotations of a round applied
-// together: G <- J^T G J, U <- U J. Lane p of pair (p, q) computes its
-// rotation, the other lanes get it by shuffles; the rotated off-diagonal
-// entry is then set to exactly 0. A pair rotates while
-// g_pq^2 > tol^2 |g_pp g_qq| and |g_pq| > 1e-17 (trace 1; below that lies
-// the Gram's own rounding). Returns the sweeps; *conv: a sweep without a
-// rotation was reached.
+// Cyclic Jacobi on the symmetric JC x JC matrix held by one warp (entries
+// >= JC are zero padding). Lane k < JC holds row k of G and of U, their
+// columns in SLOT order: g[s] = G[k][col(s)], u[s] = U[k][col(s)], U
+// starting at I. Pair q of a round is the columns in slots (2q, 2q + 1); the
+// slots advance on the circle-method ring after each round (register moves
+// with static indices), so the round body is one compact loop iteration. G is
+// first scaled by 1 / trace (eigenvectors unchanged; the 1e-17 floor below is
+// then relative to the trace). Per round: lane q computes the
+// rotation of pair q = (p, p') (p = col(2q)), every lane applies all of them
+// to its row's columns (G <- G J, U <- U J), rows p and p' exchange through
+// shuffles (G <- J^T G), and the rotated off-diagonal is set to exactly 0. A
+// pair rotates while g_pp'^2 > tol^2 |g_pp g_p'p'| and |g_pp'| > 1e-17 (below
+// that lies the Gram's own rounding). Returns the sweeps; *conv: a sweep
+// without a rotation was reached.
 template <int JC, int LC>
 __device__ __forceinline__ int bt_jacobi(double (&g)[LC], double (&u)[LC], double tol, bool* conv) {
+  constexpr int h = JC / 2;
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   double tr = 0.0;
@@ -339,71 +342,79 @@ __device__ __forceinline__ int bt_jacobi(double (&g)[LC], double (&u)[LC], doubl
 #pragma unroll
   for (int k = 0; k < JC; ++k) g[k] *= sc;
   const double fl = 1e-17, tol2 = tol * tol;
+  int colv[LC];
+#pragma unroll
+  for (int k = 0; k < LC; ++k) colv[k] = k;
   int sweep = 0;
   *conv = false;
   for (; sweep < 30; ++sweep) {
     bool anyl = false;
-#pragma unroll
+#pragma unroll 1
     for (int rnd = 0; rnd < JC - 1; ++rnd) {
-      // this lane's partner and role (static register indices only)
-      int partner = lane;
-      bool isp = true;
-      double dg = 0.0, off = 0.0;
+      // the three entries of pair q, gathered in lane q
+      double dg = 0.0, off = 0.0, dq = 0.0;
+      int myslot = 0;
 #pragma unroll
-      for (int pr = 0; pr < JC / 2; ++pr) {
-        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
-        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-        if (lane == p) { partner = q; isp = true; dg = g[p]; off = g[q]; }
-        if (lane == q) { partner = p; isp = false; dg = g[q]; off = g[p]; }
+      for (int q = 0; q < h; ++q) {
+        const int p = colv[2 * q], pp = colv[2 * q + 1];
+        const double a0 = __shfl_sync(full, g[2 * q], p);
+        const double a1 = __shfl_sync(full, g[2 * q + 1], p);
+        const double a2 = __shfl_sync(full, g[2 * q + 1], pp);
+        if (lane == q) { dg = a0; off = a1; dq = a2; }
+        if (lane == p) myslot = 2 * q;
+        if (lane == pp) myslot = 2 * q + 1;
       }
-      const double dq = __shfl_sync(full, dg, partner);
       double c = 1.0, s = 0.0;
       bool rot = false;
-      if (isp && lane < JC && off * off > tol2 * fabs(dg * dq) && fabs(off) > fl) {
+      if (lane < h && off * off > tol2 * fabs(dg * dq) && fabs(off) > fl) {
         // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0,
         // zeta = (g_qq - g_pp) / (2 g_pq): t = sgn(zeta) 2|g_pq| / (|dif| + sqrt(dif^2 + 4 g_pq^2))
         const double dif = dq - dg;
         const double sg = ((dif >= 0.0) == (off >= 0.0)) ? 1.0 : -1.0;
-        const double h2 = fma(dif, dif, 4.0 * off * off);
-        const double den = fabs(dif) + h2 * bt_rsqrt(h2);
-        const double t = sg * 2.0 * fabs(off) * bt_rcp(den);
-        c = bt_rsqrt(fma(t, t, 1.0));
+        // (IEEE sqrt and division: ~100 and ~80 cycles of latency on B200, less
+        // than fp32-seeded Newton sequences with their fp64<->fp32 conversions)
+        const double h = sqrt(fma(dif, dif, 4.0 * off * off));
+        const double t = sg * 2.0 * fabs(off) / (fabs(dif) + h);
+        c = 1.0 / sqrt(fma(t, t, 1.0));
         s = c * t;
         rot = true;
       }
       anyl |= rot;
-      {
-        const double cq = __shfl_sync(full, c, partner), sq = __shfl_sync(full, s, partner);
-        const bool rq = __shfl_sync(full, rot ? 1 : 0, partner) != 0;
-        if (!isp) { c = cq; s = sq; rot = rq; }
-      }
-      // columns: G <- G J, U <- U J (every lane its own row; pair (p, q) uses lane p's c, s)
+      // columns: G <- G J, U <- U J; this row's own pair parameters on the way
+      double myc = 1.0, mys = 0.0;
+      bool myrot = false;
 #pragma unroll
-      for (int pr = 0; pr < JC / 2; ++pr) {
-        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
-        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-        const double cc = __shfl_sync(full, c, p), ss = __shfl_sync(full, s, p);
-        const double gp = g[p], gq = g[q];
-        g[p] = cc * gp - ss * gq;
-        g[q] = ss * gp + cc * gq;
-        const double up = u[p], uq = u[q];
-        u[p] = cc * up - ss * uq;
-        u[q] = ss * up + cc * uq;
+      for (int q = 0; q < h; ++q) {
+        const double cc = __shfl_sync(full, c, q), ss = __shfl_sync(full, s, q);
+        const double gp = g[2 * q], gq = g[2 * q + 1];
+        g[2 * q] = cc * gp - ss * gq;
+        g[2 * q + 1] = ss * gp + cc * gq;
+        const double up = u[2 * q], uq = u[2 * q + 1];
+        u[2 * q] = cc * up - ss * uq;
+        u[2 * q + 1] = ss * up + cc * uq;
+        if ((myslot >> 1) == q) { myc = cc; mys = ss; }
       }
-      // rows: G <- J^T G (rows p and q of a pair exchange through shuffles)
+      myrot = __shfl_sync(full, rot ? 1 : 0, myslot >> 1) != 0;
+      // rows: G <- J^T G (the row of the slot partner through shuffles)
+      int partner = 0;
+#pragma unroll
+      for (int k = 0; k < JC; ++k)
+        if (k == (myslot ^ 1)) partner = colv[k];
+      const bool isp = (myslot & 1) == 0;
 #pragma unroll
       for (int k = 0; k < JC; ++k) {
         const double o = __shfl_sync(full, g[k], partner);
-        g[k] = isp ? (c * g[k] - s * o) : (s * o + c * g[k]);
+        g[k] = isp ? (myc * g[k] - mys * o) : (mys * o + myc * g[k]);
       }
       // the rotated pair's off-diagonal is zero by construction
+      if (myrot) {
 #pragma unroll
-      for (int pr = 0; pr < JC / 2; ++pr) {
-        const int a0 = bt_pair_a(JC, rnd, pr), b0 = bt_pair_b(JC, rnd, pr);
-        const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-        if (rot && lane == p) g[q] = 0.0;
-        if (rot && lane == q) g[p] = 0.0;
+        for (int k = 0; k < JC; ++k)
+          if (k == (myslot ^ 1)) g[k] = 0.0;
       }
+      bt_ring<JC, LC>(g);
+      bt_ring<JC, LC>(u);
+      bt_ring<JC, LC>(colv);
     }
     if (!__any_sync(full, anyl)) {
       ++sweep;
@@ -430,8 +441,6 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
   const int lds = L.lds;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned long long* stamp = a.stamps ? a.stamps + (size_t)b * 8 : nullptr;
-  if (stamp && tid == 0) stamp[0] = clock64();
   const T* A = reinterpret_cast<const T*>(a.A) + (int64_t)b * a.strideA;
   const T* Om = reinterpret_cast<const T*>(a.Om);
   // a sample whose residual is below this fraction of its norm carries no
@@ -459,26 +468,32 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (stamp && tid == 0) stamp[1] = clock64();
+  if (a.stop_after == 1) return;
   int rb = 0;
-  double vs_raw = 0.0, dummy = 0.0;
+  double vs_raw = 0.0;
+  int s_kept = 0;
   double y[RM][LC];
-  bt_ax<T, LC, RM>(sA, lds, m, n, sW, y);
-  int s_kept = bt_orth<LC, RM>(y, l, tol, red, rb, &vs_raw);
-  bt_store<T, LC, RM>(y, m, sQ);
-  __syncthreads();
-  if (stamp && tid == 0) stamp[2] = clock64();
-  for (int it = 0; it < a.q; ++it) {
-    bt_atx<T, LC, RM>(sA, lds, m, n, sQ, y);
-    bt_orth<LC, RM>(y, l, tol, red, rb, &dummy);
-    bt_store<T, LC, RM>(y, n, sW);
+  // phase 0: Q = orth(A Omega); then per power step Z = orth(A^T Q) (odd
+  // phases), Q = orth(A Z) (even phases). One call site of the (unrolled)
+  // orthonormalisation keeps the kernel's code compact.
+#pragma unroll 1
+  for (int ph = 0; ph <= 2 * a.q; ++ph) {
+    const bool ax = (ph & 1) == 0;
+    if (ax) bt_ax<T, LC, RM>(sA, lds, m, n, sW, y);
+    else bt_atx<T, LC, RM>(sA, lds, m, n, sQ, y);
+    double nr_last = 0.0;
+    const int kept = bt_orth<LC, RM>(y, l, tol, red, rb, &nr_last);
+    if (ph == 0) vs_raw = nr_last;
+    if (ax) {
+      s_kept = kept;
+      bt_store<T, LC, RM>(y, m, sQ);
+    } else {
+      bt_store<T, LC, RM>(y, n, sW);
+    }
     __syncthreads();
-    bt_ax<T, LC, RM>(sA, lds, m, n, sW, y);
-    s_kept = bt_orth<LC, RM>(y, l, tol, red, rb, &dummy);
-    bt_store<T, LC, RM>(y, m, sQ);
-    __syncthreads();
+    if (ph == 0 && a.stop_after == 2) return;
   }
-  if (stamp && tid == 0) stamp[3] = clock64();
+  if (a.stop_after == 3) return;
   // W = A^T Q (= B^T) in registers; per-warp partials of G = W^T W (upper
   // triangle, row-major packed, entry e(p, q) = p LC - p (p - 1) / 2 + q - p),
   // 16 entries per transposed warp reduction
@@ -510,7 +525,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
     }
   }
   __syncthreads();
-  if (stamp && tid == 0) stamp[4] = clock64();
+  if (a.stop_after == 4) return;
   int sweeps = 0;
   bool conv = true;
   if (warp == 0) {
@@ -541,7 +556,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
     }
   }
   __syncthreads();
-  if (stamp && tid == 0) stamp[5] = clock64();
+  if (a.stop_after == 5) return;
   // W U_B in place (rows in registers), sigma_c = || (W U_B)_c ||
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
@@ -614,7 +629,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
     }
   }
   __syncthreads();
-  if (stamp && tid == 0) stamp[6] = clock64();
+  if (a.stop_after == 6) return;
   // X = P (W U_B)^T, P = Q U_B diag(d / sigma); thread = row i of X (coalesced stores)
   T* X = reinterpret_cast<T*>(a.X) + (int64_t)b * a.strideX;
 #pragma unroll
@@ -640,10 +655,6 @@ __global__ void __launch_bounds__(BT_THREADS, 1) batched_frsvt_kernel(BtArgs a) 
       for (int c = 0; c < LC; ++c) acc = fma(pr[c], wr[c], acc);
       X[i + (int64_t)j * a.ldx] = acc;
     }
-  }
-  if (stamp) {
-    __syncthreads();
-    if (tid == 0) stamp[7] = clock64();
   }
 }
 

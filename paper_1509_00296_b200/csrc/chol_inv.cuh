@@ -31,15 +31,18 @@
 
 namespace frsvt {
 
-constexpr int CI_THREADS = 1024;
+constexpr int CI_THREADS = 1024;  // l > 64: 32 warps, 4 x 4 entries each (128 x 128)
+constexpr int CI_THREADS_S = 256;  // l <= 64: 8 warps, 8 x 2 entries each (64 x 64): 8-warp barriers
 #ifndef CI_PROF
 #define CI_PROF 0  // phase stamps (the test hook's `stamps`): build with -DCI_PROF=1
 #endif
-constexpr int CI_LD = FRSVT_LMAX;  // row stride (doubles) of the p x p work matrix
+constexpr int CI_LD = FRSVT_LMAX + 1;  // row stride (doubles) of the p x p work matrix: odd, so
+                                       // column-wise accesses (consecutive rows) are conflict free
+constexpr int CI_XMAX = (FRSVT_LMAX / 2 + 1) * (FRSVT_LMAX / 2 + 1);  // r x (p | 1) <= this
 
 __host__ __device__ constexpr size_t chol_inv_smem_bytes() {
-  // M (LMAX x CI_LD) + G12 (<= (LMAX/2)^2 when r, p > 0) + dsc + sd + 2 pivot rows + 2 pivot inverses
-  return ((size_t)FRSVT_LMAX * CI_LD + (size_t)(FRSVT_LMAX / 2) * (FRSVT_LMAX / 2) + 4 * FRSVT_LMAX + 2) *
+  // M (LMAX x CI_LD) + G12 (r x (p | 1) <= CI_XMAX when r, p > 0) + dsc + sd + 2 pivot rows + 2 pivot inverses
+  return ((size_t)FRSVT_LMAX * CI_LD + (size_t)CI_XMAX + 4 * FRSVT_LMAX + 2) *
          sizeof(double);
 }
 
@@ -57,8 +60,8 @@ __host__ __device__ constexpr size_t chol_inv_smem_bytes() {
 // latency-bound. Row mbarriers instead of the block barrier, the owner's row
 // updated first, or 8 warps with 16 rows each were all slower: the extra
 // live registers spill at the 64-register limit of 1024 threads.)
-template <typename Tq>
-__global__ void __launch_bounds__(CI_THREADS, 1)
+template <typename Tq, int NW = 32>
+__global__ void __launch_bounds__(NW * 32, 1)
 chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_dev, double tol, Tq* __restrict__ T,
                 int64_t ldt, int* __restrict__ s_out, int* __restrict__ flags, const int* __restrict__ skip,
                 unsigned long long* __restrict__ prof = nullptr, double* __restrict__ resid_last = nullptr) {
@@ -78,33 +81,37 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   CI_STAMP(0);
   extern __shared__ double cis[];
   double* M = cis;                               // p x p (row stride CI_LD)
-  double* X = M + (size_t)FRSVT_LMAX * CI_LD;    // G12, r x p row-major (X[c * p + i])
-  double* dsc = X + (FRSVT_LMAX / 2) * (FRSVT_LMAX / 2);
+  double* X = M + (size_t)FRSVT_LMAX * CI_LD;    // G12, r x p row-major (X[c * xld + i], xld = p | 1)
+  double* dsc = X + CI_XMAX;
   double* sd = dsc + FRSVT_LMAX;
   double* rowbuf = sd + FRSVT_LMAX;              // 2 x LMAX pivot rows
   double* invbuf = rowbuf + 2 * FRSVT_LMAX;      // 2 pivot inverses
+  constexpr int TI = NW == 32 ? 4 : 8, TJ = NW == 32 ? 4 : 2;  // rows w + NW i, columns L + 32 j
+  static_assert(NW * TI == FRSVT_LMAX || NW * TI == FRSVT_LMAX / 2, "tile");
+  constexpr int NT = NW * 32;
   const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;
   const int r = r_dev ? min(max(*r_dev, 0), l) : 0;
   const int p = l - r;
+  const int xld = p | 1;  // odd: the output phase reads X down a column
 
   // (1) fresh columns' norms, G12
-  for (int i = tid; i < p; i += CI_THREADS) {
+  for (int i = tid; i < p; i += NT) {
     const double g = G[(size_t)(r + i) * (l + 1)];
     if (!isfinite(g)) atomicOr(flags, FLAG_NONFINITE);
     dsc[i] = (g > 0.0 && isfinite(g)) ? 1.0 / sqrt(g) : 0.0;
   }
-  for (int idx = tid; idx < r * p; idx += CI_THREADS) {
+  for (int idx = tid; idx < r * p; idx += NT) {
     const int c = idx % r, i = idx / r;
-    X[c * p + i] = G[c + (size_t)(r + i) * l];
+    X[c * xld + i] = G[c + (size_t)(r + i) * l];
   }
   __syncthreads();
   CI_STAMP(1);
   // (2) equilibrated Schur complement, both triangles
-  for (int idx = tid; idx < p * p; idx += CI_THREADS) {
+  for (int idx = tid; idx < p * p; idx += NT) {
     const int i = idx / p, j = idx - i * p;
     if (j >= i) {
       double s = G[(r + j) + (size_t)(r + i) * l];  // G symmetric: coalesced along j
-      for (int c = 0; c < r; ++c) s = fma(-X[c * p + i], X[c * p + j], s);
+      for (int c = 0; c < r; ++c) s = fma(-X[c * xld + i], X[c * xld + j], s);
       double v = s * dsc[i] * dsc[j];
       if (!isfinite(v)) v = 0.0;
       M[i * CI_LD + j] = v;
@@ -117,17 +124,17 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   // (w + 32 i, L + 32 j) in registers; after the update the owner warp of row
   // k + 1 publishes it with 1 / S_{k+1,k+1} (double-buffered); one block
   // barrier per pivot
-  double m[4][4];
+  double m[TI][TJ];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int a = w + 32 * i, b = L + 32 * j;
+    for (int j = 0; j < TJ; ++j) {
+      const int a = w + NW * i, b = L + 32 * j;
       m[i][j] = (a < p && b < p) ? M[a * CI_LD + b] : 0.0;
     }
   if (w == 0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) rowbuf[L + 32 * j] = m[0][j];
+    for (int j = 0; j < TJ; ++j) rowbuf[L + 32 * j] = m[0][j];
   }
   if (tid == 0) invbuf[0] = (p > 0 && m[0][0] > tol) ? 1.0 / m[0][0] : 0.0;
   __syncthreads();
@@ -136,43 +143,43 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
     const double inv = invbuf[k & 1];
     const double d = rk[k];
     if (inv != 0.0) {
-      double v[4];
+      double v[TJ];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < TJ; ++j) {
         const int b = L + 32 * j;
         v[j] = (b == k) ? d + 1.0 : rk[b];  // column k: M_ak - u_a (S_kk + 1) = -u_a
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int a = w + 32 * i;
+      for (int i = 0; i < TI; ++i) {
+        const int a = w + NW * i;
         if (a > k && a < p) {
           const double u = rk[a] * inv;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) m[i][j] = fma(-u, v[j], m[i][j]);
+          for (int j = 0; j < TJ; ++j) m[i][j] = fma(-u, v[j], m[i][j]);
         }
       }
     } else {  // dropped pivot: no elimination, W_ak = 0
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int a = w + 32 * i;
+      for (int i = 0; i < TI; ++i) {
+        const int a = w + NW * i;
         if (a > k && a < p) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < TJ; ++j)
             if (L + 32 * j == k) m[i][j] = 0.0;
         }
       }
     }
     const int k1 = k + 1;
-    if (k1 < p && w == (k1 & 31)) {  // publish row k + 1 and its pivot inverse
+    if (k1 < p && w == (k1 % NW)) {  // publish row k + 1 and its pivot inverse
       double* rn = rowbuf + (k1 & 1) * FRSVT_LMAX;
-      const int i1 = k1 >> 5;
+      const int i1 = k1 / NW, j1 = k1 >> 5;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < TI; ++i) {
         if (i == i1) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < TJ; ++j) {
             rn[L + 32 * j] = m[i][j];
-            if (j == i1 && L == (k1 & 31)) invbuf[k1 & 1] = m[i][j] > tol ? 1.0 / m[i][j] : 0.0;
+            if (j == j1 && L == (k1 & 31)) invbuf[k1 & 1] = m[i][j] > tol ? 1.0 / m[i][j] : 0.0;
           }
         }
       }
@@ -180,21 +187,21 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int a = w + 32 * i, b = L + 32 * j;
+    for (int j = 0; j < TJ; ++j) {
+      const int a = w + NW * i, b = L + 32 * j;
       if (a < p && b < p) M[a * CI_LD + b] = m[i][j];
     }
   __syncthreads();
   CI_STAMP(3);
   // (4) T22 (upper, in place of S): T22[c][i] = dsc_c W_ic / sqrt(d_i), kept i
-  for (int i = tid; i < p; i += CI_THREADS) {
+  for (int i = tid; i < p; i += NT) {
     const double d = M[i * CI_LD + i];
     sd[i] = d > tol ? 1.0 / sqrt(d) : 0.0;
   }
   __syncthreads();
-  for (int idx = tid; idx < p * p; idx += CI_THREADS) {
+  for (int idx = tid; idx < p * p; idx += NT) {
     const int c = idx / p, i = idx - c * p;
     if (i >= c) M[c * CI_LD + i] = dsc[c] * (i == c ? 1.0 : M[i * CI_LD + c]) * sd[i];
   }
@@ -202,7 +209,7 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
 
   CI_STAMP(4);
   // (5) output, column-major with leading dimension ldt
-  for (int idx = tid; idx < l * l; idx += CI_THREADS) {
+  for (int idx = tid; idx < l * l; idx += NT) {
     const int j = idx / l, c = idx - j * l;  // T[c + j ldt]: consecutive threads along c
     double v = 0.0;
     if (j < p) {
@@ -210,7 +217,7 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
         const int cc = c - r;
         v = cc <= j ? M[cc * CI_LD + j] : 0.0;
       } else {
-        for (int i = 0; i <= j; ++i) v = fma(-X[c * p + i], M[i * CI_LD + j], v);
+        for (int i = 0; i <= j; ++i) v = fma(-X[c * xld + i], M[i * CI_LD + j], v);
       }
     }
     T[c + (int64_t)j * ldt] = (Tq)v;

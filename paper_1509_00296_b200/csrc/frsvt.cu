@@ -461,7 +461,7 @@ frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap
                         ldadd, h->skpart, rp_dev, dbg, sep_fix ? nullptr : h->tilecnt, skip_dev));
   TRY(post_launch(h));
   if (!sep_fix) return FRSVT_OK;
-  tc::p3_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)h->l), 128, 0, h->st>>>(
+  tc::p3_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)h->l), 512, 0, h->st>>>(
       Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev, skip_dev);
   return post_launch(h);
 }
@@ -751,7 +751,19 @@ frsvt_status apply_small(frsvt_handle* h, const T* In, int64_t rows, int64_t ldi
 // Out = In * M with a well-conditioned M (orthogonal-like): tensor cores when
 // eligible (3xTF32, ~2e-6 relative), else SIMT
 template <typename T>
+frsvt_status apply_rows(frsvt_handle* h, const T* In, int64_t rows, const T* M, T* Out, const int* r_dev) {
+  const int l = h->l;
+  const unsigned g = (unsigned)cdiv(rows, 128);
+  if (l <= 4) apply_rows_kernel<T, 4><<<g, 128, 0, h->st>>>(In, rows, rows, l, M, Out, rows, r_dev);
+  else if (l <= 8) apply_rows_kernel<T, 8><<<g, 128, 0, h->st>>>(In, rows, rows, l, M, Out, rows, r_dev);
+  else if (l <= 12) apply_rows_kernel<T, 12><<<g, 128, 0, h->st>>>(In, rows, rows, l, M, Out, rows, r_dev);
+  else apply_rows_kernel<T, 16><<<g, 128, 0, h->st>>>(In, rows, rows, l, M, Out, rows, r_dev);
+  return post_launch(h);
+}
+
+template <typename T>
 frsvt_status apply_fast(frsvt_handle* h, const T* In, int64_t rows, bool m_rows, const T* Msm, T* Out) {
+  if (h->l <= AR_LMAX) return apply_rows<T>(h, In, rows, Msm, Out, nullptr);  // narrow: one thread per row
   if constexpr (sizeof(T) == 4) {
     if (tc_small_ok(h, rows, m_rows))  // stream-K pass with K = l: whole tiles per CTA pair
       return tc_pass3<tc::MODE_AX>(h, (const float*)In, rows, rows, h->l, (const float*)Msm, h->l, (float*)Out, rows,
@@ -790,6 +802,18 @@ frsvt_status gemm_ll(frsvt_handle* h, const double* A, int ta, const double* B, 
   return post_launch(h);
 }
 
+// the explicit CholeskyQR factor of h->G into T (l x l, ld l): 8 warps up to
+// l = 64 (cheaper barriers), 32 warps above
+void launch_chol_inv(frsvt_handle* h, const int* r_dev, float* T, unsigned long long* stamps, double* resid) {
+  const int l = h->l;
+  if (l <= FRSVT_LMAX / 2)
+    chol_inv_kernel<float, 8><<<1, CI_THREADS_S, chol_inv_smem_bytes(), h->st>>>(
+        h->G, l, r_dev, 1e-12, T, l, &h->dev->s, &h->dev->flags, nullptr, stamps, resid);
+  else
+    chol_inv_kernel<float, 32><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(
+        h->G, l, r_dev, 1e-12, T, l, &h->dev->s, &h->dev->flags, nullptr, stamps, resid);
+}
+
 // CholeskyQR first pass with the explicit factor T of chol_inv_kernel (one
 // barrier per column, no triangular solve) applied by the stream-K tensor-core
 // pass. r_dev (range propagation, reading R11): In = [Q~ | Y_p]; only the
@@ -798,11 +822,10 @@ frsvt_status orth1_inv(frsvt_handle* h, const float* In, int64_t rows, float* Ou
   const int l = h->l;
   const bool sharded = m_rows && h->cfg.nranks > 1;
   TRY(gram<float>(h, In, rows, rows, sharded, r_dev));
-  chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, l, r_dev, 1e-12, (float*)h->T1, l,
-                                                                          &h->dev->s, &h->dev->flags, nullptr,
-                                                                          nullptr, h->resid_out);
+  launch_chol_inv(h, r_dev, (float*)h->T1, nullptr, h->resid_out);
   h->resid_out = nullptr;  // only the sketch's orthonormalisation reports it
   TRY(post_launch(h));
+  if (l <= AR_LMAX) return apply_rows<float>(h, In, rows, (const float*)h->T1, Out, r_dev);
   // r_dev: in place (Out == In): only the fresh columns are written; with
   // p <= 32 on the 32-column instance (the device-side choice of R11)
   if (r_dev && l > 32) {
@@ -997,8 +1020,10 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     TRY(gemm_ll<double>(h, h->G, 0, h->T2d, 0, h->Hd));
     TRY(gemm_ll<double>(h, h->T2d, 1, h->Hd, 0, h->G));
   }
-  if (h->rp != 0) {
+  if (h->rp != 0 && h->l > EW_P) {
     // warm start (R16): diagonalise the fresh block first, solve the rotated Gram
+    // (only for l > EW_P: a cold solve of an l <= 32 Gram costs fewer rounds
+    // than the 24- or 32-wide fresh-block solve it would save)
     int* flag = h->lwd + 12;  // [W, W == 24, W == 32] (lwd: [0..3] Loewdin, 4 debug, 7 sweeps scratch, 8..9 sketch)
     eig_fresh_pack_kernel<<<1, 256, 0, h->st>>>(h->G, h->l, &h->dev->r, h->ewbuf, flag);
     TRY(post_launch(h));
@@ -1298,7 +1323,8 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR(lowdin_series_kernel<float>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(lowdin_series_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(eig_jacobi_kernel, EigJacobi::smem_bytes(FRSVT_LMAX));
-  FRSVT_ATTR(chol_inv_kernel<float>, chol_inv_smem_bytes());
+  FRSVT_ATTR((chol_inv_kernel<float, 32>), chol_inv_smem_bytes());
+  FRSVT_ATTR((chol_inv_kernel<float, 8>), chol_inv_smem_bytes());
   CK(bt_set_attrs<float>());  // single-CTA path and frsvt_batched_apply
   CK(bt_set_attrs<double>());
   FRSVT_ATTR((tc::tc_pass_kernel<tc::MODE_ATQ, 32>), tc::PassSmem::total(32));
@@ -1886,9 +1912,7 @@ frsvt_status frsvt_debug_chol_inv(frsvt_handle* h, const double* G, int32_t r, v
   CK(cudaMemcpyAsync(h->G, G, sizeof(double) * h->l * h->l, cudaMemcpyDeviceToDevice, h->st));
   int* rd = h->lwd + 4;  // scratch int (lwd[0..3]: Loewdin flags)
   CK(cudaMemcpyAsync(rd, &r, sizeof(int), cudaMemcpyHostToDevice, h->st));
-  chol_inv_kernel<float><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(h->G, h->l, rd, 1e-12, (float*)T, h->l,
-                                                                          &h->dev->s, &h->dev->flags, nullptr,
-                                                                          stamps);
+  launch_chol_inv(h, rd, (float*)T, stamps, nullptr);
   TRY(post_launch(h));
   CK(cudaStreamSynchronize(h->st));
   if (s) CK(cudaMemcpy(s, &h->dev->s, sizeof(int), cudaMemcpyDeviceToHost));

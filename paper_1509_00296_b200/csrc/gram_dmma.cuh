@@ -119,21 +119,31 @@ gram_dmma_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, in
 
 // Gram of a tall NARROW matrix (l <= 16, e.g. BASELINE c3's l = 10 over
 // 76800 rows): the 8 x 8 DMMA blocks would leave most warps idle and chain
-// dependent MMAs, so here every thread owns entries (i <= j) of the upper
-// triangle and accumulates them in fp64 over 256-row chunks staged in shared
-// memory (4 independent partial sums per entry); one partial per CTA (both
+// dependent MMAs, so here threads own entries (i <= j) of the upper triangle
+// and accumulate them in fp64 over 256-row chunks staged in shared memory.
+// Thread t loads row t of the chunk (all l columns, issued together: one
+// memory latency per chunk, not one per element); with at most 64 entries
+// (l <= 10) four threads share an entry, each over a quarter of the rows,
+// and their sums are added in a fixed order. One partial per CTA (both
 // triangles), summed over CTAs by splitk_reduce_wide_kernel.
 constexpr int GS_THREADS = 256;
 constexpr int GS_ROWS = 256;
 constexpr int GS_LMAX = 16;
+constexpr int GS_LD = GS_ROWS + 1;  // odd column stride (doubles): the lanes of a warp read
+                                    // different columns at the same row without bank conflicts
 template <typename Tin>
 __global__ void __launch_bounds__(GS_THREADS)
 gram_small_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, int64_t rows_per_cta,
                   double* __restrict__ part) {
-  __shared__ double sY[GS_LMAX * GS_ROWS];  // column-major chunk
+  static_assert(GS_ROWS == GS_THREADS, "one row per thread");
+  __shared__ double sY[GS_LMAX * GS_LD];  // column-major chunk
+  __shared__ double red[3][64];
   const int ne = l * (l + 1) / 2;
-  // entry of this thread (l <= 16: at most 136 entries)
-  int ei = threadIdx.x, ii = 0, jj = 0;
+  const int ks_n = ne <= 64 ? 4 : 1;          // threads per entry
+  const int ei = ks_n == 4 ? (threadIdx.x & 63) : threadIdx.x;
+  const int ks = ks_n == 4 ? (threadIdx.x >> 6) : 0;
+  const int kr = GS_ROWS / ks_n;              // rows of the chunk per thread
+  int ii = 0, jj = 0;
   if (ei < ne) {
     int q = ei;
     while (q >= l - ii) {
@@ -146,18 +156,20 @@ gram_small_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, i
   const int64_t r0 = blockIdx.x * rows_per_cta;
   const int64_t r1 = min(rows, r0 + rows_per_cta);
   for (int64_t rc = r0; rc < r1; rc += GS_ROWS) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < GS_ROWS * l; idx += GS_THREADS) {
-      const int rr = idx % GS_ROWS, c = idx / GS_ROWS;
-      const int64_t r = rc + rr;
-      sY[c * GS_ROWS + rr] = r < r1 ? (double)Y[r + (int64_t)c * ldy] : 0.0;
-    }
+    const int64_t r = rc + threadIdx.x;
+    Tin v[GS_LMAX];
+#pragma unroll
+    for (int c = 0; c < GS_LMAX; ++c) v[c] = (c < l && r < r1) ? Y[r + (int64_t)c * ldy] : Tin(0);
+    __syncthreads();  // the previous chunk is consumed
+#pragma unroll
+    for (int c = 0; c < GS_LMAX; ++c)
+      if (c < l) sY[c * GS_LD + threadIdx.x] = (double)v[c];
     __syncthreads();
     if (ei < ne) {
-      const double* yi = sY + ii * GS_ROWS;
-      const double* yj = sY + jj * GS_ROWS;
+      const double* yi = sY + ii * GS_LD + ks * kr;
+      const double* yj = sY + jj * GS_LD + ks * kr;
 #pragma unroll 4
-      for (int k = 0; k < GS_ROWS; k += 4) {
+      for (int k = 0; k < kr; k += 4) {
         a0 = fma(yi[k], yj[k], a0);
         a1 = fma(yi[k + 1], yj[k + 1], a1);
         a2 = fma(yi[k + 2], yj[k + 2], a2);
@@ -165,8 +177,13 @@ gram_small_kernel(const Tin* __restrict__ Y, int64_t rows, int64_t ldy, int l, i
       }
     }
   }
-  if (ei < ne) {
-    const double v = (a0 + a1) + (a2 + a3);
+  double v = (a0 + a1) + (a2 + a3);
+  if (ks_n == 4) {
+    if (ks > 0 && ei < ne) red[ks - 1][ei] = v;
+    __syncthreads();
+    if (ks == 0 && ei < ne) v = ((v + red[0][ei]) + red[1][ei]) + red[2][ei];
+  }
+  if (ks == 0 && ei < ne) {
     double* P = part + (int64_t)blockIdx.x * l * l;
     P[ii + (int64_t)jj * l] = v;
     P[jj + (int64_t)ii * l] = v;

@@ -63,6 +63,40 @@ __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __
   }
 }
 
+// ---- narrow apply: Out (rows x ncols) = In (rows x l) M, l <= 16 -----------
+// M l x l column-major (ld l) in shared memory, one thread per row, FMA in T
+// (a tensor-core pass with K = l would spend its ~10 us of fixed set-up on a
+// 2 x rows x l x 4-byte stream). r_dev (range propagation, in place, reading
+// R11): columns [r, l) of Out = In Tp[:, 0 .. l-r), columns < r untouched.
+constexpr int AR_LMAX = 16;
+template <typename T, int L>
+__global__ void __launch_bounds__(128) apply_rows_kernel(const T* __restrict__ In, int64_t ldin, int64_t rows, int l,
+                                                         const T* __restrict__ M, T* Out, int64_t ldout,
+                                                         const int* __restrict__ r_dev) {
+  __shared__ T sM[L * L];  // zero padded to L x L, row k = M[k, :]
+  for (int idx = threadIdx.x; idx < L * L; idx += blockDim.x) {
+    const int k = idx / L, c = idx % L;
+    sM[idx] = (k < l && c < l) ? M[k + c * l] : T(0);
+  }
+  __syncthreads();
+  const int rsh = r_dev ? min(max(*r_dev, 0), l) : 0;
+  const int nact = l - rsh;
+  // one row per thread (grid = rows / 128): no row loop, so the compiler keeps
+  // sM in shared memory instead of hoisting all L^2 values into registers
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  T v[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) v[k] = k < l ? In[i + (int64_t)k * ldin] : T(0);
+#pragma unroll
+  for (int c = 0; c < L; ++c) {
+    T acc = T(0);
+#pragma unroll
+    for (int k = 0; k < L; ++k) acc = fma(v[k], sM[k * L + c], acc);
+    if (c < nact) Out[i + (int64_t)(rsh + c) * ldout] = acc;
+  }
+}
+
 // ---- split-K reduction (fixed order => deterministic) ----------------------
 template <typename Tp, typename Tout>
 __global__ void splitk_reduce_kernel(const Tp* __restrict__ part, int S, int M, int N,

@@ -561,10 +561,11 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 // A^T Q of a tall matrix with a narrow n): out = sum of the covering CTAs'
 // partial slots in cluster order (+ add), one block per (row tile, 8-column
 // group) so the reduction runs on many SMs instead of in the last covering
-// CTA. Same slots, order and result as the in-kernel fixup. Grid (row
-// tiles, output columns), 128 threads (one per row).
+// CTA. The same slots as the in-kernel fixup, summed in a fixed order (four
+// interleaved slot groups, then the groups): deterministic. Grid (row tiles,
+// output columns), 512 threads (128 rows x 4 slot groups; G <= 512).
 template <int NP>
-__global__ void __launch_bounds__(128) p3_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
+__global__ void __launch_bounds__(512) p3_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
                                                        const float* __restrict__ part, float* __restrict__ out,
                                                        int64_t ldo, const float* __restrict__ add, int64_t ldadd,
                                                        const int* __restrict__ rp_dev,
@@ -572,55 +573,74 @@ __global__ void __launch_bounds__(128) p3_fixup_kernel(int Mtot, int Ktot, int N
   if (skip_dev && *skip_dev) return;  // the pass was skipped: nothing to sum
   constexpr int CL = 2;
   __shared__ int64_t soff[256];
-  __shared__ int ncov;
+  __shared__ int wcnt[16];
   const int nch = (Ktot + BK - 1) / BK;
   const int mtiles = (Mtot + 127) / 128;
   const int mgroups = (mtiles + CL - 1) / CL;
   const int64_t total = (int64_t)mgroups * nch;
   const int tile = blockIdx.x;
   const int wt = tile / CL, crank = tile % CL;
-  if (threadIdx.x == 0) {
-    const int64_t t0 = (int64_t)wt * nch, t1 = t0 + nch;
-    int c0 = (int)((t0 * G) / total);
-    while (c0 > 0 && sk_range_begin(total, G, c0) > t0) --c0;
-    while (sk_range_begin(total, G, c0 + 1) <= t0) ++c0;
-    int c1 = c0;
-    while (c1 + 1 < G && sk_range_begin(total, G, c1 + 1) < t1) ++c1;
-    const bool whole = (c0 == c1) && sk_range_begin(total, G, c0) <= t0 && sk_range_begin(total, G, c0 + 1) >= t1;
-    int k = 0;
-    if (!whole) {
-      for (int cc = c0; cc <= c1 && k < 256; ++cc) {
-        const int64_t b = sk_range_begin(total, G, cc);
-        if (sk_range_begin(total, G, cc + 1) <= b) continue;
-        soff[k++] = ((int64_t)(cc * CL + crank) * P3_SLOTS + ((b >= t0) ? 0 : 1)) * 128 * NP;
-      }
-    }
-    ncov = k;
+  // the slots covering this tile, in cluster order: thread cc examines
+  // cluster cc's stream-K range [b0, b1) (G <= blockDim), then an ordered
+  // compaction (a serial scan by one thread costs two 64-bit divisions per
+  // cluster, ~15 us for 74 clusters)
+  const int64_t t0 = (int64_t)wt * nch, t1 = t0 + nch;
+  const int cc = threadIdx.x, wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  bool has = false, whole = false;
+  int64_t off = 0;
+  if (cc < G) {
+    const int64_t b0 = sk_range_begin(total, G, cc), b1 = sk_range_begin(total, G, cc + 1);
+    has = b1 > b0 && b0 < t1 && b1 > t0;
+    whole = has && b0 <= t0 && b1 >= t1;
+    off = ((int64_t)(cc * CL + crank) * P3_SLOTS + ((b0 >= t0) ? 0 : 1)) * 128 * NP;
   }
+  const unsigned bal = __ballot_sync(0xffffffffu, has);
+  if (ln == 0) wcnt[wp] = __popc(bal);
+  const int anywhole = __syncthreads_or(whole ? 1 : 0);
+  int kbase = 0, nc = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (w < wp) kbase += wcnt[w];
+    nc += wcnt[w];
+  }
+  if (has) soff[kbase + __popc(bal & ((1u << ln) - 1u))] = off;
   __syncthreads();
-  const int nc = ncov;
+  if (anywhole) nc = 0;
   if (nc == 0) return;  // written directly by the pass
   const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
-  const int c = blockIdx.y;  // one output column per block, one row per thread
-  const int row = threadIdx.x, gm = tile * 128 + row;
-  if (gm >= Mtot || row >= 128) return;
+  // one output column per block; thread (g, row): row of the tile, slot group
+  // g of FX_G (slots g, g + FX_G, ...), the groups summed in order afterwards
+  // (deterministic). With ~150 slots per tile (narrow A^T Q: every cluster
+  // touches the few tiles) the per-thread chain is nc / FX_G loads, 8 in flight.
+  constexpr int FX_G = 4;
+  __shared__ float gsum[FX_G - 1][128];
+  const int c = blockIdx.y;
+  const int row = threadIdx.x & 127, g = threadIdx.x >> 7, gm = tile * 128 + row;
+  const bool live = gm < Mtot;
   if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
-    if (add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+    if (g == 0 && live && add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
     return;
   }
   const float* base = part + (int64_t)(c - rsh) * 128 + row;
   float acc = 0.f;
-  int k = 0;
-  for (; k + 8 <= nc; k += 8) {  // 8 independent loads in flight, summed in slot order
-    float v[8];
+  if (live) {
+    int k = g;
+    for (; k + 7 * FX_G < nc; k += 8 * FX_G) {
+      float v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + soff[k + u]);
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + soff[k + u * FX_G]);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc += v[u];
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; k < nc; k += FX_G) acc += __ldcg(base + soff[k]);
   }
-  for (; k < nc; ++k) acc += __ldcg(base + soff[k]);
-  if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
-  out[gm + (int64_t)c * ldo] = acc;
+  if (g > 0) gsum[g - 1][row] = acc;
+  __syncthreads();
+  if (g == 0 && live) {
+#pragma unroll
+    for (int q = 0; q < FX_G - 1; ++q) acc += gsum[q][row];
+    if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
+    out[gm + (int64_t)c * ldo] = acc;
+  }
 }
 
 // B operand split of a TERMS = 2 pass: Bh = rna_tf32(x) (fp32, ld ldh) and
