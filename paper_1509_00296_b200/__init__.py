@@ -57,12 +57,14 @@ def _ld(x, rows, dtype, name):
     return x.stride(1)
 
 
-def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None):
+def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None, X=None):
     """frsvt_batched_apply: X[b] = FRSVT(A[b]) for a batch of small fp32
     matrices (one CTA each). A: (batch, m, n) CUDA fp32 with each matrix
     column-major (A[b].stride() == (1, ld)); Omega: n x l column-major. tau: a
-    float or a (batch,) tensor; w: (l,) weights. Returns X (batch, m, n, same
-    layout), r (batch,) int32, sigma (batch, l) float64."""
+    float or a (batch,) tensor; w: (l,) weights. X (optional): the output,
+    (batch, m, n) fp32 with column-major matrices (any ld >= m, any batch
+    stride); allocated when None. Returns X, r (batch,) int32, sigma (batch, l)
+    float64."""
     if A.dim() != 3 or A.dtype != torch.float32 or A.device.type != "cuda":
         raise ValueError("A must be a (batch, m, n) CUDA fp32 tensor")
     batch, m, n = A.shape
@@ -76,7 +78,11 @@ def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None):
     lda, sA = A.stride(2), A.stride(0)
     Om = colmajor(Omega.to(device=A.device, dtype=torch.float32))
     l = Om.shape[1]
-    X = torch.empty((batch, n, m), dtype=torch.float32, device=A.device).transpose(1, 2)
+    if X is None:
+        X = torch.empty((batch, n, m), dtype=torch.float32, device=A.device).transpose(1, 2)
+    elif (X.shape != A.shape or X.dtype != torch.float32 or X.device != A.device or X.stride(1) != 1
+          or X.stride(2) < max(1, m)):
+        raise ValueError("X must be a (batch, m, n) fp32 tensor on A's device with column-major matrices")
     r = torch.empty(batch, dtype=torch.int32, device=A.device)
     sig = torch.empty((batch, l), dtype=torch.float64, device=A.device)
     wmode, tau_s, tau_p, w_p = 0, 0.0, None, None
@@ -90,7 +96,7 @@ def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None):
     else:
         tau_s = float(tau)
     st = stream if stream is not None else torch.cuda.current_stream()
-    for t in (A, Om) + ((wt,) if w is not None else ()) + ((tt,) if tau_p is not None else ()):
+    for t in (A, Om, X) + ((wt,) if w is not None else ()) + ((tt,) if tau_p is not None else ()):
         t.record_stream(st)  # kept alive for the asynchronous kernel on `st`
     _check("frsvt_batched_apply", lib.frsvt_batched_apply(
         int(batch), int(m), int(n), int(l), int(q), ctypes.c_void_p(A.data_ptr()), int(lda), int(sA),
