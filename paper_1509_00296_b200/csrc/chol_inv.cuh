@@ -86,7 +86,8 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   double* sd = dsc + FRSVT_LMAX;
   double* rowbuf = sd + FRSVT_LMAX;              // 2 x LMAX pivot rows
   double* invbuf = rowbuf + 2 * FRSVT_LMAX;      // 2 pivot inverses
-  constexpr int TI = NW == 32 ? 4 : 8, TJ = NW == 32 ? 4 : 2;  // rows w + NW i, columns L + 32 j
+  // rows w + NW i, columns L + 32 j: 32 warps 4 x 4, 16 warps 8 x 4 (128 x 128); 8 warps 8 x 2 (64 x 64)
+  constexpr int TI = NW == 32 ? 4 : 8, TJ = NW == 8 ? 2 : 4;
   static_assert(NW * TI == FRSVT_LMAX || NW * TI == FRSVT_LMAX / 2, "tile");
   constexpr int NT = NW * 32;
   const int tid = threadIdx.x, w = tid >> 5, L = tid & 31;

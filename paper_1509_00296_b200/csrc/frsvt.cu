@@ -810,7 +810,7 @@ void launch_chol_inv(frsvt_handle* h, const int* r_dev, float* T, unsigned long 
     chol_inv_kernel<float, 8><<<1, CI_THREADS_S, chol_inv_smem_bytes(), h->st>>>(
         h->G, l, r_dev, 1e-12, T, l, &h->dev->s, &h->dev->flags, nullptr, stamps, resid);
   else
-    chol_inv_kernel<float, 32><<<1, CI_THREADS, chol_inv_smem_bytes(), h->st>>>(
+    chol_inv_kernel<float, 16><<<1, 512, chol_inv_smem_bytes(), h->st>>>(
         h->G, l, r_dev, 1e-12, T, l, &h->dev->s, &h->dev->flags, nullptr, stamps, resid);
 }
 
@@ -1323,7 +1323,7 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR(lowdin_series_kernel<float>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(lowdin_series_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(eig_jacobi_kernel, EigJacobi::smem_bytes(FRSVT_LMAX));
-  FRSVT_ATTR((chol_inv_kernel<float, 32>), chol_inv_smem_bytes());
+  FRSVT_ATTR((chol_inv_kernel<float, 16>), chol_inv_smem_bytes());
   FRSVT_ATTR((chol_inv_kernel<float, 8>), chol_inv_smem_bytes());
   CK(bt_set_attrs<float>());  // single-CTA path and frsvt_batched_apply
   CK(bt_set_attrs<double>());
