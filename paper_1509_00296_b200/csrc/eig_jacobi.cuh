@@ -90,6 +90,165 @@ __device__ __forceinline__ int eig_col_at(bool top, int q, int k, int L2) {
   return c + 1;
 }
 
+// Per-launch state of the round body (see eig_jacobi_kernel).
+struct EigRoundCtx {
+  double* meta;
+  double* abuf;
+  double* mbox;
+  double tol2, tsmall, tstop2;
+  int l, nw, warp, lane, pj, Rr;
+  bool b4, b3;
+  int rho_x, rho_y;  // ring indices of this lane's parameter pair
+  bool bigoff;       // an off-diagonal above tol_stop was measured this sweep
+  int rotated;
+};
+
+// One round of the sweep at ring phase t (compile time). The ring advance is
+// a renaming, not a copy: logical top slot j lives in X[(j - t) & 3] and
+// bottom slot j in Y[(j + t) & 3], so the outgoing top slot 3 / bottom slot 0
+// registers take the incoming columns and the other six slots move without a
+// register move (the round loop is unrolled by 4; the sweep ends at phase 3
+// and is renamed back once). Only warp 0 (the fixed column T[0]) and the last
+// warp (T[h-1] -> B[h-1]) copy one column each.
+template <int t>
+__device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[EIG_PPW][4], EigRoundCtx& c,
+                                          int rnd) {
+  constexpr int PPW = EIG_PPW;
+  static_assert(PPW == 4, "the renaming period is the pairs per warp");
+#define XL(j) X[((j) - t) & 3]
+#define YL(j) Y[((j) + t) & 3]
+  const int lane = c.lane, warp = c.warp;
+  // partial dots, then a reduce-scatter: the 8-lane group p ends with the
+  // full (stored) dot of pair p
+  double gp[PPW];
+#pragma unroll
+  for (int j = 0; j < PPW; ++j) {
+    double s = XL(j)[0] * YL(j)[0];
+#pragma unroll
+    for (int e = 1; e < 4; ++e) s = fma(XL(j)[e], YL(j)[e], s);
+    gp[j] = s;
+  }
+  double k0 = c.b4 ? gp[2] : gp[0], k1 = c.b4 ? gp[3] : gp[1];
+  k0 += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[0] : gp[2], 16);
+  k1 += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[1] : gp[3], 16);
+  double gm = c.b3 ? k1 : k0;
+  gm += __shfl_xor_sync(0xffffffffu, c.b3 ? k0 : k1, 8);
+  gm += __shfl_xor_sync(0xffffffffu, gm, 4);
+  gm += __shfl_xor_sync(0xffffffffu, gm, 2);
+  gm += __shfl_xor_sync(0xffffffffu, gm, 1);
+  // rotation parameters of pair pj, lane-parallel over the 4 pairs
+  {
+    const int cx = c.rho_x + 1, cy = c.rho_y + 1;  // column = (ring index - round) mod R, + 1
+    if (c.rho_x >= 0) c.rho_x = (c.rho_x == 0) ? c.Rr - 1 : c.rho_x - 1;
+    c.rho_y = (c.rho_y == 0) ? c.Rr - 1 : c.rho_y - 1;
+    double* meta = c.meta;
+    const double2 mx01 = *reinterpret_cast<const double2*>(meta + 4 * cx);
+    const double2 my01 = *reinterpret_cast<const double2*>(meta + 4 * cy);
+    const double dinx = meta[4 * cx + 2], diny = meta[4 * cy + 2];
+    const double al = mx01.x, be = my01.x, dxv = mx01.y, dyv = my01.y;
+    const double g = gm * dxv * dyv;  // true dot
+    const double abv = al * be, gg = g * g;
+    double a = 0.0, b = 0.0;
+    const bool rot = (cx < c.l) && (cy < c.l) && al > 0.0 && be > 0.0 && gg > c.tol2 * abv;
+    if (rot) {
+      // convergence measure (see the header): relative to the larger
+      // column when the smaller one is clearly below the threshold
+      const double mxn = fmax(al, be);
+      const double den = fmin(al, be) >= c.tsmall ? abv : mxn * mxn;
+      c.bigoff |= gg > c.tstop2 * den;
+      // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
+      // in fp32 (~1e-7 relative) for |zeta| <= 1e4, else t = 1/(2|zeta|) in fp64
+      // (relative error < 1e-8 + that of the approximate reciprocal): any t
+      // defines an exact rotation once c, s are consistent with it, an
+      // approximate angle only leaves a ~1e-7 fraction of g for the next sweep
+      const double zeta = 0.5 * (be - al) * eig_rcp_approx(g);
+      const double azd = fabs(zeta);
+      double tt;
+      if (azd <= 1e4) {
+        const float az = (float)azd;
+        const float z1 = fmaf(az, az, 1.0f);
+        tt = (double)__frcp_rn(fmaf(z1, rsqrtf(z1), az));
+      } else {
+        tt = 0.5 * eig_rcp_approx(azd);
+      }
+      const double tn = zeta >= 0.0 ? tt : -tt;
+      // c = 1/sqrt(1 + t^2) to full precision: fp32 seed, two Newton steps
+      const double q1 = fma(tn, tn, 1.0), hq = -0.5 * q1;
+      double cs = (double)rsqrtf((float)q1);
+      cs = cs * fma(hq * cs, cs, 1.5);
+      cs = cs * fma(hq * cs, cs, 1.5);
+      const double sn = cs * tn, ic = q1 * cs;  // ic = 1/c
+      a = tn * dyv * dinx;
+      b = tn * dxv * diny;
+      c.rotated = 1;
+      if ((lane & 7) == 0) {
+        const double c2 = cs * cs, s2 = sn * sn, cs2 = 2.0 * cs * sn * g;
+        meta[4 * cx + 0] = fma(c2, al, fma(s2, be, -cs2));
+        meta[4 * cx + 1] = cs * dxv;
+        meta[4 * cx + 2] = ic * dinx;
+        meta[4 * cy + 0] = fma(s2, al, fma(c2, be, cs2));
+        meta[4 * cy + 1] = cs * dyv;
+        meta[4 * cy + 2] = ic * diny;
+      }
+    }
+    if ((lane & 7) == 0) {
+      c.abuf[(warp * PPW + c.pj) * 2 + 0] = a;
+      c.abuf[(warp * PPW + c.pj) * 2 + 1] = b;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < PPW; ++j) {
+    const double2 abj = *reinterpret_cast<const double2*>(c.abuf + (warp * PPW + j) * 2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double xv = XL(j)[e], yv = YL(j)[e];
+      XL(j)[e] = fma(-abj.x, yv, xv);
+      YL(j)[e] = fma(abj.y, xv, yv);
+    }
+  }
+  // ---- advance the ring by one position --------------------------------
+  // after it (phase t + 1) the new top slot 0 is register X[(3 - t) & 3] (the
+  // old top slot 3) and the new bottom slot 3 is Y[t & 3] (the old bottom 0)
+  const int nw = c.nw;
+  double* mb = c.mbox + (size_t)(rnd & 1) * nw * 2 * 128;
+  if (warp + 1 < nw) {  // last top slot -> warp + 1
+    double* outT = mb + (size_t)(warp * 2 + 0) * 128;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) outT[32 * e + lane] = XL(3)[e];
+  }
+  if (warp > 0) {  // first bottom slot -> warp - 1
+    double* outB = mb + (size_t)(warp * 2 + 1) * 128;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) outB[32 * e + lane] = YL(0)[e];
+  }
+  if (warp == 0) {  // T[0] stays, B[0] -> T[1] (and, with one warp, T[h-1] -> B[h-1])
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double f = X[(0 - t) & 3][e], y0 = Y[t & 3][e], x3 = X[(3 - t) & 3][e];
+      X[(3 - t) & 3][e] = f;
+      X[(0 - t) & 3][e] = y0;
+      if (nw == 1) Y[t & 3][e] = x3;
+    }
+  } else if (warp == nw - 1) {  // T[h-1] -> B[h-1]
+#pragma unroll
+    for (int e = 0; e < 4; ++e) Y[t & 3][e] = X[(3 - t) & 3][e];
+  }
+  __syncthreads();
+  if (warp > 0) {  // new top slot 0 <- warp - 1's last top slot
+    const double* inT = mb + (size_t)((warp - 1) * 2 + 0) * 128;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) X[(3 - t) & 3][e] = inT[32 * e + lane];
+  }
+  if (warp + 1 < nw) {  // new bottom slot 3 <- warp + 1's first bottom slot
+    const double* inB = mb + (size_t)((warp + 1) * 2 + 1) * 128;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) Y[t & 3][e] = inB[32 * e + lane];
+  }
+#undef XL
+#undef YL
+}
+
 __global__ void __launch_bounds__(512, 1)
 eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict__ t_dev, double t_host,
                   int t_mode, double tol_rot, double tol_stop, int max_sweeps, double* __restrict__ sigma,
@@ -170,13 +329,23 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
     meta[4 * c + 3] = 0.0;
   }
 
-  const double tol2 = tol_rot * tol_rot;
+  EigRoundCtx ctx;
+  ctx.meta = meta;
+  ctx.abuf = abuf;
+  ctx.mbox = mbox;
+  ctx.tol2 = tol_rot * tol_rot;
   // |m|^2 below which a column is clearly under the threshold (sigma < t/2,
   // |G v|^2 = lambda^2 < t^4/16); 0 without a scalar threshold
-  const double tsmall = t2 > 0.0 ? t2 * t2 * (1.0 / 16.0) : 0.0;
-
-  const int pj = lane >> 3;  // the pair this lane computes parameters for
-  const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+  ctx.tsmall = t2 > 0.0 ? t2 * t2 * (1.0 / 16.0) : 0.0;
+  ctx.tstop2 = tol_stop > 0.0 ? tol_stop * tol_stop : 0.0;
+  ctx.l = l;
+  ctx.nw = nw;
+  ctx.warp = warp;
+  ctx.lane = lane;
+  ctx.pj = lane >> 3;  // the pair this lane computes parameters for
+  ctx.b4 = (lane & 16) != 0;
+  ctx.b3 = (lane & 8) != 0;
+  ctx.Rr = L2 - 1;
   int sweep = 0;
   bool converged = false;
   int rnd_base = 0;  // rounds elapsed (ring offset)
@@ -219,162 +388,51 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
       }
       __syncthreads();
     }
-    double maxrel = 0.0;
-    int rotated = 0;
-    // ring indices of this lane's parameter pair, advanced by one per round
-    const int Rr = L2 - 1;
-    int rho_x = (q0 + pj == 0) ? -1 : q0 + pj - 1, rho_y = L2 - 2 - (q0 + pj);
+    ctx.bigoff = false;
+    ctx.rotated = 0;
     {
-      const int k = rnd_base % Rr;
+      const int pj = ctx.pj, Rr = ctx.Rr, k = rnd_base % Rr;
+      int rho_x = (q0 + pj == 0) ? -1 : q0 + pj - 1, rho_y = L2 - 2 - (q0 + pj);
       if (rho_x >= 0) rho_x = (rho_x - k + Rr) % Rr;
       rho_y = (rho_y - k + Rr) % Rr;
+      ctx.rho_x = rho_x;
+      ctx.rho_y = rho_y;
     }
-    for (int rr = 0; rr < L2 - 1; ++rr) {
-      const int rnd = rnd_base + rr;
-      // partial dots, then a reduce-scatter: the 8-lane group p ends with the
-      // full (stored) dot of pair p
-      double gp[PPW];
+    // L2 - 1 = 8 nw - 1 rounds = G4 groups of 4, the last one cut after 3
+    const int G4 = L2 / 4;
+    for (int g4 = 0; g4 < G4; ++g4) {
+      const int rnd = rnd_base + 4 * g4;
+      eig_round<0>(x, y, ctx, rnd);
+      eig_round<1>(x, y, ctx, rnd + 1);
+      eig_round<2>(x, y, ctx, rnd + 2);
+      if (g4 == G4 - 1) break;
+      eig_round<3>(x, y, ctx, rnd + 3);
+    }
+    // phase 3 -> 0: top slot j is x[(j + 1) & 3], bottom slot j is y[(j + 3) & 3]
 #pragma unroll
-      for (int j = 0; j < PPW; ++j) {
-        double s = x[j][0] * y[j][0];
-#pragma unroll
-        for (int e = 1; e < 4; ++e) s = fma(x[j][e], y[j][e], s);
-        gp[j] = s;
-      }
-      double k0 = b4 ? gp[2] : gp[0], k1 = b4 ? gp[3] : gp[1];
-      k0 += __shfl_xor_sync(0xffffffffu, b4 ? gp[0] : gp[2], 16);
-      k1 += __shfl_xor_sync(0xffffffffu, b4 ? gp[1] : gp[3], 16);
-      double gm = b3 ? k1 : k0;
-      gm += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
-      gm += __shfl_xor_sync(0xffffffffu, gm, 4);
-      gm += __shfl_xor_sync(0xffffffffu, gm, 2);
-      gm += __shfl_xor_sync(0xffffffffu, gm, 1);
-      // rotation parameters of pair pj, lane-parallel over the 4 pairs
-      {
-        const int cx = rho_x + 1, cy = rho_y + 1;  // column = (ring index - round) mod R, + 1
-        if (rho_x >= 0) rho_x = (rho_x == 0) ? Rr - 1 : rho_x - 1;
-        rho_y = (rho_y == 0) ? Rr - 1 : rho_y - 1;
-        const double2 mx01 = *reinterpret_cast<const double2*>(meta + 4 * cx);
-        const double2 my01 = *reinterpret_cast<const double2*>(meta + 4 * cy);
-        const double dinx = meta[4 * cx + 2], diny = meta[4 * cy + 2];
-        const double al = mx01.x, be = my01.x, dxv = mx01.y, dyv = my01.y;
-        const double g = gm * dxv * dyv;  // true dot
-        const double abv = al * be, gg = g * g;
-        double a = 0.0, b = 0.0;
-        const bool rot = (cx < l) && (cy < l) && al > 0.0 && be > 0.0 && gg > tol2 * abv;
-        if (rot) {
-          // convergence measure (see the header): relative to the larger
-          // column when the smaller one is clearly below the threshold
-          const double mxn = fmax(al, be);
-          const double den = fmin(al, be) >= tsmall ? abv : mxn * mxn;
-          maxrel = fmax(maxrel, gg * eig_rcp_approx(den));
-          // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
-          // to ~1e-7 relative: any t defines an exact rotation once c, s are
-          // consistent with it, an approximate angle only leaves a ~1e-7 fraction
-          // of g for the next sweep
-          const double zeta = 0.5 * (be - al) * eig_rcp_approx(g);
-          const double az = fmin(fabs(zeta), 1e150);
-          const double z1 = fma(az, az, 1.0);
-          const double tt = eig_rcp_approx(az + z1 * eig_rsqrt_approx(z1));
-          const double t = zeta >= 0.0 ? tt : -tt;
-          // c = 1/sqrt(1 + t^2) to full precision (two Newton steps)
-          const double q1 = fma(t, t, 1.0);
-          double c = eig_rsqrt_approx(q1);
-          c = c * fma(-0.5 * q1 * c, c, 1.5);
-          c = c * fma(-0.5 * q1 * c, c, 1.5);
-          const double s = c * t, ic = q1 * c;  // ic = 1/c
-          a = t * dyv * dinx;
-          b = t * dxv * diny;
-          rotated = 1;
-          if ((lane & 7) == 0) {
-            const double c2 = c * c, s2 = s * s, cs2 = 2.0 * c * s * g;
-            meta[4 * cx + 0] = fma(c2, al, fma(s2, be, -cs2));
-            meta[4 * cx + 1] = c * dxv;
-            meta[4 * cx + 2] = ic * dinx;
-            meta[4 * cy + 0] = fma(s2, al, fma(c2, be, cs2));
-            meta[4 * cy + 1] = c * dyv;
-            meta[4 * cy + 2] = ic * diny;
-          }
-        }
-        if ((lane & 7) == 0) {
-          abuf[(warp * PPW + pj) * 2 + 0] = a;
-          abuf[(warp * PPW + pj) * 2 + 1] = b;
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < PPW; ++j) {
-        const double2 abj = *reinterpret_cast<const double2*>(abuf + (warp * PPW + j) * 2);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double xv = x[j][e], yv = y[j][e];
-          x[j][e] = fma(-abj.x, yv, xv);
-          y[j][e] = fma(abj.y, xv, yv);
-        }
-      }
-      // ---- advance the ring by one position -------------------------------
-      double* mb = mbox + (size_t)(rnd & 1) * nw * 2 * 128;
-      if (warp + 1 < nw) {  // last top slot -> warp + 1
-        double* outT = mb + (size_t)(warp * 2 + 0) * 128;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) outT[32 * e + lane] = x[PPW - 1][e];
-      }
-      if (warp > 0) {  // first bottom slot -> warp - 1
-        double* outB = mb + (size_t)(warp * 2 + 1) * 128;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) outB[32 * e + lane] = y[0][e];
-      }
-      double tmp[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) tmp[e] = y[0][e];
-#pragma unroll
-      for (int j = 0; j < PPW - 1; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) y[j][e] = y[j + 1][e];
-      if (warp == nw - 1) {  // T[h-1] -> B[h-1]
-#pragma unroll
-        for (int e = 0; e < 4; ++e) y[PPW - 1][e] = x[PPW - 1][e];
-      }
-#pragma unroll
-      for (int j = PPW - 1; j >= 2; --j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[j][e] = x[j - 1][e];
-      if (warp == 0) {  // T[0] stays, B[0] -> T[1]
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[1][e] = tmp[e];
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[1][e] = x[0][e];
-      }
-      __syncthreads();
-      if (warp > 0) {  // T[q0] <- warp - 1's last top slot
-        const double* inT = mb + (size_t)((warp - 1) * 2 + 0) * 128;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[0][e] = inT[32 * e + lane];
-      }
-      if (warp + 1 < nw) {  // B[q0 + PPW - 1] <- warp + 1's first bottom slot
-        const double* inB = mb + (size_t)((warp + 1) * 2 + 1) * 128;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) y[PPW - 1][e] = inB[32 * e + lane];
-      }
+    for (int e = 0; e < 4; ++e) {
+      const double x0 = x[0][e], y3 = y[3][e];
+      x[0][e] = x[1][e];
+      x[1][e] = x[2][e];
+      x[2][e] = x[3][e];
+      x[3][e] = x0;
+      y[3][e] = y[2][e];
+      y[2][e] = y[1][e];
+      y[1][e] = y[0][e];
+      y[0][e] = y3;
     }
     rnd_base += L2 - 1;
     // ---- sweep verdict -----------------------------------------------------
-    maxrel = warp_max(maxrel);
-    rotated = __any_sync(0xffffffffu, rotated);
+    const int big = __any_sync(0xffffffffu, ctx.bigoff);
+    const int rotated = __any_sync(0xffffffffu, ctx.rotated);
     if (lane == 0) {
-      red_d[warp] = maxrel;
-      red_i[warp] = rotated;
+      red_i[warp] = rotated | (big << 1);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double mr = 0.0;
       int any = 0;
-      for (int w = 0; w < nw; ++w) {
-        mr = fmax(mr, red_d[w]);
-        any |= red_i[w];
-      }
-      stop_sh = (!any) || (tol_stop > 0.0 && mr <= tol_stop * tol_stop);
+      for (int w = 0; w < nw; ++w) any |= red_i[w];
+      stop_sh = !(any & 1) || (tol_stop > 0.0 && !(any & 2));
     }
     __syncthreads();
     if (stop_sh) {
