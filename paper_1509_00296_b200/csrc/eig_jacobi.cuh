@@ -14,15 +14,17 @@
 // stays, the ring T[1] -> ... -> T[h-1] -> B[h-1] -> ... -> B[0] -> T[1]
 // advances one position per round, and pair q is (T[q], B[q]). Column c >= 1
 // starts at ring index c - 1, so the column in every slot at every round is
-// a closed form (eig_col_at). Warp w owns the 4 pairs q = 4w .. 4w + 3; lane
-// j holds rows j, j+32, j+64, j+96 of its 8 columns in registers. Advancing
-// the ring is a register shift inside a warp; only two columns per warp cross
-// to a neighbour warp, through a double-buffered shared-memory mailbox (one
-// block barrier per round).
+// a closed form (eig_col_at). Warp w owns the 8 pairs q = 8w .. 8w + 7; lane
+// j holds rows j, j+32, j+64, j+96 of its 16 columns in registers (8 warps of
+// up to 255 registers at l = 120: fewer warps issuing the per-round parameter
+// chain than 4 pairs per warp on 15 warps). Advancing the ring is a register
+// renaming inside a warp (eig_round); only two columns per warp cross to a
+// neighbour warp, through a double-buffered shared-memory mailbox (one block
+// barrier per round).
 //
-// Per round and warp: 4 partial dots, a reduce-scatter that leaves the dot of
-// pair p in lanes 8p .. 8p+7, the rotation parameters of the 4 pairs computed
-// lane-parallel, then the rotations. Rotations are applied in scaled form
+// Per round and warp: 8 partial dots, a reduce-scatter that leaves the dot of
+// pair p in lanes 4p .. 4p+3, the rotation parameters of the 8 pairs computed
+// lane-parallel (branch-free), then the rotations. Rotations are applied in scaled form
 // (column c is stored as x~ with true column d_c x~): x~' = x~ - a y~,
 // y~' = y~ + b x~ with a = t d_y / d_x, b = t d_x / d_y, d' = c d — two FMAs
 // per element pair instead of four. The per-column metadata (true squared
@@ -55,17 +57,20 @@
 
 namespace frsvt {
 
-constexpr int EIG_PPW = 4;  // pairs per warp
+// pairs per warp: 8 (two renaming halves of 4; 8 warps of up to 255
+// registers at l = 120) above l = 40, else 4 (fewer rounds for small l: the
+// sweep has 2 * PPW * warps - 1 rounds)
+__host__ __device__ constexpr int eig_ppw(int l) { return l > 40 ? 8 : 4; }
 
 struct EigJacobi {
   static int warps(int l) {
-    const int per = 2 * EIG_PPW;
+    const int per = 2 * eig_ppw(l);
     return (l + per - 1) / per;
   }
-  // mailbox [2][nw][2][128] + metadata [128][4] + a/b [nw][4][2]
+  // mailbox [2][nw][2][128] + metadata [128][4] + a/b [nw][PPW][2]
   static size_t smem_bytes(int l) {
     const int nw = warps(l);
-    return ((size_t)2 * nw * 2 * 128 + (size_t)FRSVT_LMAX * 4 + (size_t)nw * EIG_PPW * 2) * sizeof(double) + 64;
+    return ((size_t)2 * nw * 2 * 128 + (size_t)FRSVT_LMAX * 4 + (size_t)nw * eig_ppw(l) * 2) * sizeof(double) + 64;
   }
 };
 
@@ -97,29 +102,30 @@ struct EigRoundCtx {
   double* mbox;
   double tol2, tsmall, tstop2;
   int l, nw, warp, lane, pj, Rr;
-  bool b4, b3;
+  bool b4, b3, b2;
   int rho_x, rho_y;  // ring indices of this lane's parameter pair
   bool bigoff;       // an off-diagonal above tol_stop was measured this sweep
-  int rotated;
+  bool rotated;
+  bool precise;      // fp64-level tolerance: c to full precision (two Newton steps)
 };
 
-// One round of the sweep at ring phase t (compile time). The ring advance is
-// a renaming, not a copy: logical top slot j lives in X[(j - t) & 3] and
-// bottom slot j in Y[(j + t) & 3], so the outgoing top slot 3 / bottom slot 0
-// registers take the incoming columns and the other six slots move without a
-// register move (the round loop is unrolled by 4; the sweep ends at phase 3
-// and is renamed back once). Only warp 0 (the fixed column T[0]) and the last
-// warp (T[h-1] -> B[h-1]) copy one column each.
-template <int t>
-__device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[EIG_PPW][4], EigRoundCtx& c,
-                                          int rnd) {
-  constexpr int PPW = EIG_PPW;
-  static_assert(PPW == 4, "the renaming period is the pairs per warp");
-#define XL(j) X[((j) - t) & 3]
-#define YL(j) Y[((j) + t) & 3]
+// One round of the sweep at ring phase t (compile time). The PPW top / PPW
+// bottom slots of a warp are PPW / 4 halves of 4; inside a half the ring advance
+// is a register renaming, not a copy: logical top slot j lives in
+// x[(j & 4) + (((j & 3) - t) & 3)] and bottom slot j in
+// y[(j & 4) + (((j & 3) + t) & 3)], so per round only the two columns that
+// cross between the halves are copied (the round loop is unrolled by 4; the
+// sweep ends at phase 3 and is renamed back once). Warp 0 (the fixed column
+// T[0]) and the last warp (T[h-1] -> B[h-1]) copy one more column each.
+template <int t, int PPW>
+__device__ __forceinline__ void eig_round(double (&X)[PPW][4], double (&Y)[PPW][4], EigRoundCtx& c, int rnd) {
+  static_assert(PPW == 4 || PPW == 8, "renaming halves of 4 pairs");
+  constexpr int H = PPW / 4;
+#define XL(j) X[((j) & 4) + ((((j) & 3) - t) & 3)]
+#define YL(j) Y[((j) & 4) + ((((j) & 3) + t) & 3)]
   const int lane = c.lane, warp = c.warp;
-  // partial dots, then a reduce-scatter: the 8-lane group p ends with the
-  // full (stored) dot of pair p
+  // partial dots, then a reduce-scatter: the (32 / PPW)-lane group p ends
+  // with the full (stored) dot of pair p
   double gp[PPW];
 #pragma unroll
   for (int j = 0; j < PPW; ++j) {
@@ -128,15 +134,36 @@ __device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[E
     for (int e = 1; e < 4; ++e) s = fma(XL(j)[e], YL(j)[e], s);
     gp[j] = s;
   }
-  double k0 = c.b4 ? gp[2] : gp[0], k1 = c.b4 ? gp[3] : gp[1];
-  k0 += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[0] : gp[2], 16);
-  k1 += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[1] : gp[3], 16);
-  double gm = c.b3 ? k1 : k0;
-  gm += __shfl_xor_sync(0xffffffffu, c.b3 ? k0 : k1, 8);
-  gm += __shfl_xor_sync(0xffffffffu, gm, 4);
+  double gm;
+  if constexpr (PPW == 8) {
+    double k4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k4[i] = c.b4 ? gp[4 + i] : gp[i];
+      k4[i] += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[i] : gp[4 + i], 16);
+    }
+    double k2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      k2[i] = c.b3 ? k4[2 + i] : k4[i];
+      k2[i] += __shfl_xor_sync(0xffffffffu, c.b3 ? k4[i] : k4[2 + i], 8);
+    }
+    gm = c.b2 ? k2[1] : k2[0];
+    gm += __shfl_xor_sync(0xffffffffu, c.b2 ? k2[0] : k2[1], 4);
+  } else {
+    double k2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      k2[i] = c.b4 ? gp[2 + i] : gp[i];
+      k2[i] += __shfl_xor_sync(0xffffffffu, c.b4 ? gp[i] : gp[2 + i], 16);
+    }
+    gm = c.b3 ? k2[1] : k2[0];
+    gm += __shfl_xor_sync(0xffffffffu, c.b3 ? k2[0] : k2[1], 8);
+    gm += __shfl_xor_sync(0xffffffffu, gm, 4);
+  }
   gm += __shfl_xor_sync(0xffffffffu, gm, 2);
   gm += __shfl_xor_sync(0xffffffffu, gm, 1);
-  // rotation parameters of pair pj, lane-parallel over the 4 pairs
+  // rotation parameters of pair pj, lane-parallel over the PPW pairs
   {
     const int cx = c.rho_x + 1, cy = c.rho_y + 1;  // column = (ring index - round) mod R, + 1
     if (c.rho_x >= 0) c.rho_x = (c.rho_x == 0) ? c.Rr - 1 : c.rho_x - 1;
@@ -148,40 +175,40 @@ __device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[E
     const double al = mx01.x, be = my01.x, dxv = mx01.y, dyv = my01.y;
     const double g = gm * dxv * dyv;  // true dot
     const double abv = al * be, gg = g * g;
-    double a = 0.0, b = 0.0;
     const bool rot = (cx < c.l) && (cy < c.l) && al > 0.0 && be > 0.0 && gg > c.tol2 * abv;
-    if (rot) {
-      // convergence measure (see the header): relative to the larger
-      // column when the smaller one is clearly below the threshold
-      const double mxn = fmax(al, be);
-      const double den = fmin(al, be) >= c.tsmall ? abv : mxn * mxn;
-      c.bigoff |= gg > c.tstop2 * den;
-      // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
-      // in fp32 (~1e-7 relative) for |zeta| <= 1e4, else t = 1/(2|zeta|) in fp64
-      // (relative error < 1e-8 + that of the approximate reciprocal): any t
-      // defines an exact rotation once c, s are consistent with it, an
-      // approximate angle only leaves a ~1e-7 fraction of g for the next sweep
-      const double zeta = 0.5 * (be - al) * eig_rcp_approx(g);
-      const double azd = fabs(zeta);
-      double tt;
-      if (azd <= 1e4) {
-        const float az = (float)azd;
-        const float z1 = fmaf(az, az, 1.0f);
-        tt = (double)__frcp_rn(fmaf(z1, rsqrtf(z1), az));
-      } else {
-        tt = 0.5 * eig_rcp_approx(azd);
-      }
-      const double tn = zeta >= 0.0 ? tt : -tt;
-      // c = 1/sqrt(1 + t^2) to full precision: fp32 seed, two Newton steps
-      const double q1 = fma(tn, tn, 1.0), hq = -0.5 * q1;
-      double cs = (double)rsqrtf((float)q1);
-      cs = cs * fma(hq * cs, cs, 1.5);
-      cs = cs * fma(hq * cs, cs, 1.5);
-      const double sn = cs * tn, ic = q1 * cs;  // ic = 1/c
-      a = tn * dyv * dinx;
-      b = tn * dxv * diny;
-      c.rotated = 1;
-      if ((lane & 7) == 0) {
+    // branch-free: every lane evaluates the rotation (safe operands where it
+    // does not rotate, t = 0 there), so the warp never splits
+    // convergence measure (see the header): relative to the larger
+    // column when the smaller one is clearly below the threshold
+    const double mxn = fmax(al, be);
+    const double den = fmin(al, be) >= c.tsmall ? abv : mxn * mxn;
+    c.bigoff |= rot && gg > c.tstop2 * den;
+    // t = tan(theta) = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al)/(2g),
+    // in fp32 (~1e-7 relative) for |zeta| <= 1e4, else t = 1/(2|zeta|) in fp64
+    // (relative error < 1e-8 + that of the approximate reciprocal): any t
+    // defines an exact rotation once c, s are consistent with it, an
+    // approximate angle only leaves a ~1e-7 fraction of g for the next sweep
+    const double zeta = 0.5 * (be - al) * eig_rcp_approx(rot ? g : 1.0);
+    const double azd = fabs(zeta);
+    const float az = (float)fmin(azd, 1e4);
+    const float z1 = fmaf(az, az, 1.0f);
+    float tf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(tf) : "f"(fmaf(z1, rsqrtf(z1), az)));
+    const double tt = azd <= 1e4 ? (double)tf : 0.5 * eig_rcp_approx(fmax(azd, 1e4));
+    const double tn = rot ? (zeta >= 0.0 ? tt : -tt) : 0.0;
+    // c = 1/sqrt(1 + t^2) consistent with t: fp32 seed and one Newton step
+    // (~2^-45), a second for fp64 handles (c only scales the column: its error
+    // reaches sigma, not U_B)
+    const double q1 = fma(tn, tn, 1.0), hq = -0.5 * q1;
+    double cs = (double)rsqrtf((float)q1);
+    cs = cs * fma(hq * cs, cs, 1.5);
+    if (c.precise) cs = cs * fma(hq * cs, cs, 1.5);
+    const double sn = cs * tn, ic = q1 * cs;  // ic = 1/c
+    const double a = tn * dyv * dinx;
+    const double b = tn * dxv * diny;
+    c.rotated |= rot;
+    if ((lane & (32 / PPW - 1)) == 0) {
+      if (rot) {
         const double c2 = cs * cs, s2 = sn * sn, cs2 = 2.0 * cs * sn * g;
         meta[4 * cx + 0] = fma(c2, al, fma(s2, be, -cs2));
         meta[4 * cx + 1] = cs * dxv;
@@ -190,8 +217,6 @@ __device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[E
         meta[4 * cy + 1] = cs * dyv;
         meta[4 * cy + 2] = ic * diny;
       }
-    }
-    if ((lane & 7) == 0) {
       c.abuf[(warp * PPW + c.pj) * 2 + 0] = a;
       c.abuf[(warp * PPW + c.pj) * 2 + 1] = b;
     }
@@ -208,54 +233,72 @@ __device__ __forceinline__ void eig_round(double (&X)[EIG_PPW][4], double (&Y)[E
     }
   }
   // ---- advance the ring by one position --------------------------------
-  // after it (phase t + 1) the new top slot 0 is register X[(3 - t) & 3] (the
-  // old top slot 3) and the new bottom slot 3 is Y[t & 3] (the old bottom 0)
+  // registers of phase t (half hh): top slot 4hh + 3 = X[4hh + ((3 - t) & 3)],
+  // top 0 = X[(-t) & 3]; bottom slot 4hh = Y[4hh + (t & 3)]. At phase t + 1
+  // the register of old top 4hh + 3 is new top 4hh (<- old top 4hh - 1, or
+  // warp - 1 for hh = 0) and that of old bottom 4hh is new bottom 4hh + 3
+  // (<- old bottom 4hh + 4, or warp + 1 for the last half).
+  constexpr int X3 = (3 - t) & 3, X0 = (0 - t) & 3, Y0 = t & 3;
+  constexpr int XL7 = 4 * (H - 1) + X3, YL4 = 4 * (H - 1) + Y0;  // last half's top out / bottom in
   const int nw = c.nw;
   double* mb = c.mbox + (size_t)(rnd & 1) * nw * 2 * 128;
+  double x7[4], y0[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    x7[e] = X[XL7][e];
+    y0[e] = Y[Y0][e];
+  }
   if (warp + 1 < nw) {  // last top slot -> warp + 1
     double* outT = mb + (size_t)(warp * 2 + 0) * 128;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) outT[32 * e + lane] = XL(3)[e];
+    for (int e = 0; e < 4; ++e) outT[32 * e + lane] = x7[e];
   }
   if (warp > 0) {  // first bottom slot -> warp - 1
     double* outB = mb + (size_t)(warp * 2 + 1) * 128;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) outB[32 * e + lane] = YL(0)[e];
+    for (int e = 0; e < 4; ++e) outB[32 * e + lane] = y0[e];
   }
-  if (warp == 0) {  // T[0] stays, B[0] -> T[1] (and, with one warp, T[h-1] -> B[h-1])
+#pragma unroll
+  for (int hh = H - 1; hh >= 1; --hh)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) X[4 * hh + X3][e] = X[4 * (hh - 1) + X3][e];  // top 4hh - 1 -> top 4hh
+#pragma unroll
+  for (int hh = 0; hh + 1 < H; ++hh)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) Y[4 * hh + Y0][e] = Y[4 * (hh + 1) + Y0][e];  // bottom 4hh + 4 -> bottom 4hh + 3
+  if (warp == 0) {  // T[0] stays, B[0] -> T[1]
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const double f = X[(0 - t) & 3][e], y0 = Y[t & 3][e], x3 = X[(3 - t) & 3][e];
-      X[(3 - t) & 3][e] = f;
-      X[(0 - t) & 3][e] = y0;
-      if (nw == 1) Y[t & 3][e] = x3;
+      X[X3][e] = X[X0][e];
+      X[X0][e] = y0[e];
     }
-  } else if (warp == nw - 1) {  // T[h-1] -> B[h-1]
+  }
+  if (warp == nw - 1) {  // T[h-1] -> B[h-1]
 #pragma unroll
-    for (int e = 0; e < 4; ++e) Y[t & 3][e] = X[(3 - t) & 3][e];
+    for (int e = 0; e < 4; ++e) Y[YL4][e] = x7[e];
   }
   __syncthreads();
   if (warp > 0) {  // new top slot 0 <- warp - 1's last top slot
     const double* inT = mb + (size_t)((warp - 1) * 2 + 0) * 128;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) X[(3 - t) & 3][e] = inT[32 * e + lane];
+    for (int e = 0; e < 4; ++e) X[X3][e] = inT[32 * e + lane];
   }
-  if (warp + 1 < nw) {  // new bottom slot 3 <- warp + 1's first bottom slot
+  if (warp + 1 < nw) {  // new last bottom slot <- warp + 1's first bottom slot
     const double* inB = mb + (size_t)((warp + 1) * 2 + 1) * 128;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) Y[t & 3][e] = inB[32 * e + lane];
+    for (int e = 0; e < 4; ++e) Y[YL4][e] = inB[32 * e + lane];
   }
 #undef XL
 #undef YL
 }
 
-__global__ void __launch_bounds__(512, 1)
+template <int PPW>
+__global__ void __launch_bounds__(PPW == 8 ? 256 : 512, 1)
 eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict__ t_dev, double t_host,
                   int t_mode, double tol_rot, double tol_stop, int max_sweeps, double* __restrict__ sigma,
                   double* __restrict__ UB, int* __restrict__ sweeps_out, int* __restrict__ flags,
                   const int* __restrict__ run_if = nullptr) {
   if (run_if && !*run_if) return;  // (warm-start block solve, eig_warm.cuh) not needed
-  constexpr int PPW = EIG_PPW;
   extern __shared__ double esm[];
   const int nw = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -334,6 +377,7 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
   ctx.abuf = abuf;
   ctx.mbox = mbox;
   ctx.tol2 = tol_rot * tol_rot;
+  ctx.precise = tol_rot < 1e-12;
   // |m|^2 below which a column is clearly under the threshold (sigma < t/2,
   // |G v|^2 = lambda^2 < t^4/16); 0 without a scalar threshold
   ctx.tsmall = t2 > 0.0 ? t2 * t2 * (1.0 / 16.0) : 0.0;
@@ -342,9 +386,10 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
   ctx.nw = nw;
   ctx.warp = warp;
   ctx.lane = lane;
-  ctx.pj = lane >> 3;  // the pair this lane computes parameters for
+  ctx.pj = lane / (32 / PPW);  // the pair this lane computes parameters for
   ctx.b4 = (lane & 16) != 0;
   ctx.b3 = (lane & 8) != 0;
+  ctx.b2 = (lane & 4) != 0;
   ctx.Rr = L2 - 1;
   int sweep = 0;
   bool converged = false;
@@ -389,7 +434,7 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
       __syncthreads();
     }
     ctx.bigoff = false;
-    ctx.rotated = 0;
+    ctx.rotated = false;
     {
       const int pj = ctx.pj, Rr = ctx.Rr, k = rnd_base % Rr;
       int rho_x = (q0 + pj == 0) ? -1 : q0 + pj - 1, rho_y = L2 - 2 - (q0 + pj);
@@ -402,25 +447,27 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
     const int G4 = L2 / 4;
     for (int g4 = 0; g4 < G4; ++g4) {
       const int rnd = rnd_base + 4 * g4;
-      eig_round<0>(x, y, ctx, rnd);
-      eig_round<1>(x, y, ctx, rnd + 1);
-      eig_round<2>(x, y, ctx, rnd + 2);
+      eig_round<0, PPW>(x, y, ctx, rnd);
+      eig_round<1, PPW>(x, y, ctx, rnd + 1);
+      eig_round<2, PPW>(x, y, ctx, rnd + 2);
       if (g4 == G4 - 1) break;
-      eig_round<3>(x, y, ctx, rnd + 3);
+      eig_round<3, PPW>(x, y, ctx, rnd + 3);
     }
-    // phase 3 -> 0: top slot j is x[(j + 1) & 3], bottom slot j is y[(j + 3) & 3]
+    // phase 3 -> 0: in each half, top slot j is x[(j + 1) & 3], bottom slot j is y[(j + 3) & 3]
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const double x0 = x[0][e], y3 = y[3][e];
-      x[0][e] = x[1][e];
-      x[1][e] = x[2][e];
-      x[2][e] = x[3][e];
-      x[3][e] = x0;
-      y[3][e] = y[2][e];
-      y[2][e] = y[1][e];
-      y[1][e] = y[0][e];
-      y[0][e] = y3;
-    }
+    for (int hh = 0; hh < PPW; hh += 4)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double x0 = x[hh][e], y3 = y[hh + 3][e];
+        x[hh][e] = x[hh + 1][e];
+        x[hh + 1][e] = x[hh + 2][e];
+        x[hh + 2][e] = x[hh + 3][e];
+        x[hh + 3][e] = x0;
+        y[hh + 3][e] = y[hh + 2][e];
+        y[hh + 2][e] = y[hh + 1][e];
+        y[hh + 1][e] = y[hh][e];
+        y[hh][e] = y3;
+      }
     rnd_base += L2 - 1;
     // ---- sweep verdict -----------------------------------------------------
     const int big = __any_sync(0xffffffffu, ctx.bigoff);
@@ -501,6 +548,20 @@ eig_jacobi_kernel(const double* __restrict__ G, int l, const double* __restrict_
     *sweeps_out = sweep;
     if (!converged) atomicOr(flags, FLAG_NOCONV);
   }
+}
+
+// host launcher: the pairs-per-warp instance of l (eig_ppw), one CTA on st
+inline void eig_jacobi_launch(cudaStream_t st, const double* G, int l, const double* t_dev, double t_host, int t_mode,
+                              double tol_rot, double tol_stop, int max_sweeps, double* sigma, double* UB,
+                              int* sweeps_out, int* flags, const int* run_if = nullptr) {
+  const int nw = EigJacobi::warps(l);
+  const size_t smem = EigJacobi::smem_bytes(l);
+  if (eig_ppw(l) == 8)
+    eig_jacobi_kernel<8><<<1, 32 * nw, smem, st>>>(G, l, t_dev, t_host, t_mode, tol_rot, tol_stop, max_sweeps, sigma,
+                                                     UB, sweeps_out, flags, run_if);
+  else
+    eig_jacobi_kernel<4><<<1, 32 * nw, smem, st>>>(G, l, t_dev, t_host, t_mode, tol_rot, tol_stop, max_sweeps, sigma,
+                                                     UB, sweeps_out, flags, run_if);
 }
 
 }  // namespace frsvt

@@ -999,14 +999,12 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
 frsvt_status launch_eig_jacobi(frsvt_handle* h, const double* G, double* sigma, double* UB, int t_mode,
                                double t_host, const double* t_dev) {
   const int l = h->l;
-  const int nw = EigJacobi::warps(l);
-  const size_t smem = EigJacobi::smem_bytes(l);
   // fp64 handles: rotate down to 1e-15 relative, confirm with a clean sweep;
   // fp32 handles: rotate to 1e-9, stop after a sweep that measured <= 1e-4 (R3)
   const double tol_rot = h->esz == 8 ? 1e-15 : 1e-9;
   const double tol_stop = h->esz == 8 ? 0.0 : 1e-4;
-  eig_jacobi_kernel<<<1, 32 * nw, smem, h->st>>>(G, l, t_dev, t_host, t_mode, tol_rot, tol_stop, 40, sigma, UB,
-                                                 &h->dev->sweeps, &h->dev->flags);
+  eig_jacobi_launch(h->st, G, l, t_dev, t_host, t_mode, tol_rot, tol_stop, 40, sigma, UB, &h->dev->sweeps,
+                    &h->dev->flags);
   return post_launch(h);
 }
 
@@ -1035,11 +1033,11 @@ frsvt_status small_svd(frsvt_handle* h, const T* A, int64_t lda, int t_mode = 0,
     // solve refines), fp64 handles to 1e-15
     const double ew_rot = h->esz == 4 ? 1e-9 : 1e-15, ew_stop = h->esz == 4 ? 1e-4 : 0.0;
     // the fresh-block solve at width 24 or 32 (whichever the device-side p selected)
-    eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(24), EigJacobi::smem_bytes(24), h->st>>>(
-        Gpad, 24, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 1);
+    eig_jacobi_launch(h->st, Gpad, 24, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags,
+                      flag + 1);
     TRY(post_launch(h));
-    eig_jacobi_kernel<<<1, 32 * EigJacobi::warps(EW_P), EigJacobi::smem_bytes(EW_P), h->st>>>(
-        Gpad, EW_P, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags, flag + 2);
+    eig_jacobi_launch(h->st, Gpad, EW_P, nullptr, 0.0, 0, ew_rot, ew_stop, 40, sigf, Uf, h->lwd + 7, &h->dev->flags,
+                      flag + 2);
     TRY(post_launch(h));
     eig_fresh_rotate_kernel<<<(unsigned)cdiv((int64_t)h->l * h->l, 256), 256, 0, h->st>>>(h->G, h->l, &h->dev->r,
                                                                                           Uf, flag, G2);
@@ -1322,7 +1320,8 @@ frsvt_status set_smem_attrs() {
   FRSVT_ATTR(lowdin_sq_kernel, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(lowdin_series_kernel<float>, lowdin_smem_bytes(FRSVT_LMAX));
   FRSVT_ATTR(lowdin_series_kernel<double>, lowdin_smem_bytes(FRSVT_LMAX));
-  FRSVT_ATTR(eig_jacobi_kernel, EigJacobi::smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(eig_jacobi_kernel<8>, EigJacobi::smem_bytes(FRSVT_LMAX));
+  FRSVT_ATTR(eig_jacobi_kernel<4>, EigJacobi::smem_bytes(40));
   FRSVT_ATTR((chol_inv_kernel<float, 16>), chol_inv_smem_bytes());
   FRSVT_ATTR((chol_inv_kernel<float, 8>), chol_inv_smem_bytes());
   CK(bt_set_attrs<float>());  // single-CTA path and frsvt_batched_apply

@@ -45,12 +45,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&dG, 8 * l * l); cudaMalloc(&dU, 8 * l * l); cudaMalloc(&dsig, 8 * l);
   cudaMalloc(&dsw, 4); cudaMalloc(&df, 4); cudaMemset(df, 0, 4);
   cudaMemcpy(dG, G.data(), 8 * l * l, cudaMemcpyHostToDevice);
-  const int nwarp = EigJacobi::warps(l);
-  const size_t smem = EigJacobi::smem_bytes(l);
-  cudaFuncSetAttribute(eig_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   auto run = [&]() {
-    eig_jacobi_kernel<<<1, nwarp * 32, smem>>>(dG, l, nullptr, 0.0, 0, 1e-15, 0.0, kind == 1 ? 40 : sweeps, dsig, dU, dsw, df,
-                                               nullptr);
+    eig_jacobi_launch(0, dG, l, nullptr, 0.0, 0, 1e-15, 0.0, kind == 1 ? 40 : sweeps, dsig, dU, dsw, df, nullptr);
   };
   for (int i = 0; i < 3; ++i) run();
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
