@@ -461,8 +461,12 @@ frsvt_status launch_p3(frsvt_handle* h, const CUtensorMap& mA, const CUtensorMap
                         ldadd, h->skpart, rp_dev, dbg, sep_fix ? nullptr : h->tilecnt, skip_dev));
   TRY(post_launch(h));
   if (!sep_fix) return FRSVT_OK;
-  tc::p3_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)h->l), 512, 0, h->st>>>(
-      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev, skip_dev);
+  // columns per block: as many as keep ~2 waves of 4 blocks per SM (each
+  // block first scans the covering clusters' ranges, once for all its columns)
+  int fx_c = (int)((int64_t)mtiles * h->l / (8 * (int64_t)h->nsm));
+  fx_c = fx_c < 1 ? 1 : (fx_c > tc::P3_FX_C ? tc::P3_FX_C : fx_c);
+  tc::p3_fixup_kernel<NP><<<dim3((unsigned)mtiles, (unsigned)cdiv(h->l, fx_c)), 512, 0, h->st>>>(
+      Mtot, Ktot, h->l, G, h->skpart, out, ldo, add, ldadd, rp_dev, skip_dev, fx_c);
   return post_launch(h);
 }
 

@@ -559,17 +559,18 @@ tc_pass3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 
 // Tiles split between MANY clusters (a pass with few output tiles, e.g. the
 // A^T Q of a tall matrix with a narrow n): out = sum of the covering CTAs'
-// partial slots in cluster order (+ add), one block per (row tile, 8-column
-// group) so the reduction runs on many SMs instead of in the last covering
-// CTA. The same slots as the in-kernel fixup, summed in a fixed order (four
-// interleaved slot groups, then the groups): deterministic. Grid (row tiles,
-// output columns), 512 threads (128 rows x 4 slot groups; G <= 512).
+// partial slots in cluster order (+ add), one block per (row tile, fx_c <=
+// P3_FX_C output columns) so the reduction runs on many SMs instead of in the
+// last covering CTA. The same slots as the in-kernel fixup, summed in a fixed order
+// (four interleaved slot groups, then the groups): deterministic. Grid (row
+// tiles, column groups), 512 threads (128 rows x 4 slot groups; G <= 512).
+constexpr int P3_FX_C = 8;
 template <int NP>
 __global__ void __launch_bounds__(512) p3_fixup_kernel(int Mtot, int Ktot, int Nvalid, int G,
                                                        const float* __restrict__ part, float* __restrict__ out,
                                                        int64_t ldo, const float* __restrict__ add, int64_t ldadd,
                                                        const int* __restrict__ rp_dev,
-                                                       const int* __restrict__ skip_dev) {
+                                                       const int* __restrict__ skip_dev, int fx_c) {
   if (skip_dev && *skip_dev) return;  // the pass was skipped: nothing to sum
   constexpr int CL = 2;
   __shared__ int64_t soff[256];
@@ -607,39 +608,45 @@ __global__ void __launch_bounds__(512) p3_fixup_kernel(int Mtot, int Ktot, int N
   if (anywhole) nc = 0;
   if (nc == 0) return;  // written directly by the pass
   const int rsh = rp_dev ? min(max(*rp_dev, 0), Nvalid) : 0;
-  // one output column per block; thread (g, row): row of the tile, slot group
-  // g of FX_G (slots g, g + FX_G, ...), the groups summed in order afterwards
+  // fx_c output columns per block (the slot scan above is paid once per
+  // block, not per column; the launch picks fx_c so that ~2 waves of blocks
+  // remain); thread (g, row): row of the tile, slot group g of
+  // FX_G (slots g, g + FX_G, ...), the groups summed in order afterwards
   // (deterministic). With ~150 slots per tile (narrow A^T Q: every cluster
   // touches the few tiles) the per-thread chain is nc / FX_G loads, 8 in flight.
   constexpr int FX_G = 4;
   __shared__ float gsum[FX_G - 1][128];
-  const int c = blockIdx.y;
   const int row = threadIdx.x & 127, g = threadIdx.x >> 7, gm = tile * 128 + row;
   const bool live = gm < Mtot;
-  if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
-    if (g == 0 && live && add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
-    return;
-  }
-  const float* base = part + (int64_t)(c - rsh) * 128 + row;
-  float acc = 0.f;
-  if (live) {
-    int k = g;
-    for (; k + 7 * FX_G < nc; k += 8 * FX_G) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + soff[k + u * FX_G]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
+  for (int cj = 0; cj < fx_c; ++cj) {
+    const int c = blockIdx.y * fx_c + cj;  // block-uniform
+    if (c >= Nvalid) break;
+    if (rp_dev && c < rsh) {  // carried column (copied unless the output is in place)
+      if (g == 0 && live && add) out[gm + (int64_t)c * ldo] = add[gm + (int64_t)c * ldadd];
+      continue;
     }
-    for (; k < nc; k += FX_G) acc += __ldcg(base + soff[k]);
-  }
-  if (g > 0) gsum[g - 1][row] = acc;
-  __syncthreads();
-  if (g == 0 && live) {
+    const float* base = part + (int64_t)(c - rsh) * 128 + row;
+    float acc = 0.f;
+    if (live) {
+      int k = g;
+      for (; k + 7 * FX_G < nc; k += 8 * FX_G) {
+        float v[8];
 #pragma unroll
-    for (int q = 0; q < FX_G - 1; ++q) acc += gsum[q][row];
-    if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
-    out[gm + (int64_t)c * ldo] = acc;
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + soff[k + u * FX_G]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; k < nc; k += FX_G) acc += __ldcg(base + soff[k]);
+    }
+    if (g > 0) gsum[g - 1][row] = acc;
+    __syncthreads();
+    if (g == 0 && live) {
+#pragma unroll
+      for (int q = 0; q < FX_G - 1; ++q) acc += gsum[q][row];
+      if (add && !rp_dev) acc += add[gm + (int64_t)c * ldadd];
+      out[gm + (int64_t)c * ldo] = acc;
+    }
+    __syncthreads();  // gsum is reused by the next column
   }
 }
 
