@@ -80,6 +80,18 @@ def _profile_facts(cfg_name, kind):
     return d.get("bytes_per_launch"), d.get("tensor_pipe_pct")
 
 
+def _finite(x):
+    """the JSON line with every non-finite float (an ncu metric without data)
+    as null: strict JSON"""
+    if isinstance(x, dict):
+        return {k: _finite(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [_finite(v) for v in x]
+    if isinstance(x, float) and not math.isfinite(x):
+        return None
+    return x
+
+
 def alg_bytes_per_unit(cfg):
     """SURVEY §8(d) algorithmic HBM bytes per unit of work (elem = dtype size):
     FRSVT call (2q+3) m n elem (2q+2 reads of A, 1 write of X); iALM iteration
@@ -534,7 +546,7 @@ def main():
     else:
         line = run_ours(args, ws, rank, local, dist)
     if line is not None:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -84,6 +84,13 @@ typedef struct {
 /* frsvt_config.options bits */
 #define FRSVT_OPT_FUSED_SKETCH 1u /* rpca_alm_step: form the next call's fresh sketch in the fused
                                      epilogue (see rpca_alm_step); fp32, range propagation, one rank */
+#define FRSVT_OPT_TF32_OMEGA 2u   /* fp32 handles: every drawn Omega entry is rounded to tf32 (round to
+                                     nearest, ties away: the fp32 draw with its low 13 mantissa bits
+                                     cleared after adding 0x1000), so the tensor-core sketch multiplies
+                                     A by Omega exactly. A
+                                     different test matrix, not a different method: the oracle takes
+                                     the same rounded Omega (synth.omega(..., tf32=True)). Omega set by
+                                     frsvt_set_omega is used as given. EINVAL on fp64 handles. */
 
 /* Host-side report of one call (filling it synchronises the stream). */
 typedef struct {

@@ -13,12 +13,12 @@ import os
 
 import torch
 
-from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, FrsvtConfig, FrsvtInfo,
-                   RpcaState, load_library, status_string)
+from ._abi import (FRSVT_F32, FRSVT_F64, FRSVT_LMAX, FRSVT_OPT_FUSED_SKETCH, FRSVT_OPT_TF32_OMEGA, FrsvtConfig,
+                   FrsvtInfo, RpcaState, load_library, status_string)
 
 __all__ = ["Frsvt", "FrsvtError", "LoopbackGroup", "batched_apply", "lib", "library_path", "colmajor", "W_EXPLICIT",
-           "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH", "FLAG_NONFINITE", "FLAG_NOCONV",
-           "FLAG_NONMONOTONE_W", "FLAG_SINGLE_CTA"]
+           "W_RECIPROCAL", "W_REWEIGHTED", "FRSVT_OPT_FUSED_SKETCH", "FRSVT_OPT_TF32_OMEGA", "FLAG_NONFINITE",
+           "FLAG_NOCONV", "FLAG_NONMONOTONE_W", "FLAG_SINGLE_CTA"]
 
 W_EXPLICIT, W_RECIPROCAL, W_REWEIGHTED = 0, 1, 2
 # frsvt_info.flags bits (include/frsvt.h FRSVT_FLAG_*)

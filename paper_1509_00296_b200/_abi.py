@@ -28,6 +28,7 @@ class FrsvtConfig(ctypes.Structure):
                 ("group", ctypes.c_void_p)]
 
 FRSVT_OPT_FUSED_SKETCH = 1
+FRSVT_OPT_TF32_OMEGA = 2
 
 
 class FrsvtInfo(ctypes.Structure):

@@ -123,6 +123,7 @@ struct frsvt_handle {
   double* ewbuf;     // Gpad, Uf (32 x 32 each), sigma_f (32), G2 (l x l)
   int single_cta;    // the last frsvt_apply ran on the single-CTA path (FRSVT_FLAG_SINGLE_CTA)
   int fs;            // 1: fuse the next call's fresh sketch into the iALM composition (FRSVT_OPT_FUSED_SKETCH)
+  int om_tf32;       // 1: drawn Omega entries rounded to tf32 (FRSVT_OPT_TF32_OMEGA)
   int ap_on, ap_a, ap_jump, ap_b, ap_l0;  // adaptive rank prediction (Eq. 7), frsvt_set_adaptive_rank
   int keep;          // partial SVT of the current rpca step (rpca_state.keep; 0 for frsvt_apply*)
   double* resid_out;  // where the next sketch orthonormalisation reports its last-sample residual
@@ -934,7 +935,7 @@ frsvt_status range_finder(frsvt_handle* h, const T* A, int64_t lda, int q, uint3
   if constexpr (sizeof(T) == 4) rp_front = use_carry && tc_eligible(h, A, lda);
   omega_kernel<T><<<grid1d(h->n * l), 256, 0, h->st>>>((T*)h->Om, h->n, l, &h->dev->r, use_carry ? 1 : 0,
                                                        h->cfg.seed, stream + (uint32_t)call, ov, h->n,
-                                                       rp_front ? 1 : 0, pmax);
+                                                       rp_front ? 1 : 0, pmax, h->om_tf32);
   // the first orthonormalisation of the sketch reports the residual of its
   // last sample (tensor path), the Prop. 4 by-product
   CK(cudaMemsetAsync(&h->dev->varsig_raw, 0, sizeof(double), h->st));
@@ -1283,7 +1284,8 @@ frsvt_status rpca_impl(frsvt_handle* h, rpca_state* st, int finalize, double* re
       if (fs_next) {
         omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 1,
                                                                     h->cfg.seed, 1000u + (uint32_t)h->call, nullptr,
-                                                                    h->n, 1, h->ap_on ? &h->dev->p_ap : nullptr);
+                                                                    h->n, 1, h->ap_on ? &h->dev->p_ap : nullptr,
+                                                                    h->om_tf32);
         TRY(post_launch(h));
         CK(cudaMemcpyAsync(h->Y, h->Qt, (size_t)h->m * h->l * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
       }
@@ -1479,6 +1481,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
   if (!cfg) return FRSVT_EINVAL;
   const frsvt_config& c = *cfg;
   if (c.dtype != FRSVT_F32 && c.dtype != FRSVT_F64) return FRSVT_EINVAL;
+  if ((c.options & FRSVT_OPT_TF32_OMEGA) && c.dtype != FRSVT_F32) return FRSVT_EINVAL;
   if (c.m_local < 1 || c.n < 1 || c.m_global < c.m_local || c.row0 < 0 || c.row0 + c.m_local > c.m_global)
     return FRSVT_EINVAL;
   if (c.l < 1 || c.l > FRSVT_LMAX || c.l > c.n || c.l > c.m_global || c.l > c.m_local) return FRSVT_EINVAL;
@@ -1573,6 +1576,7 @@ frsvt_status frsvt_create(const frsvt_config* cfg, void* cuda_stream, frsvt_hand
       return FRSVT_ENOMEM;
     }
     h->fs = (c.options & FRSVT_OPT_FUSED_SKETCH) ? 1 : 0;
+    h->om_tf32 = (c.options & FRSVT_OPT_TF32_OMEGA) ? 1 : 0;
     h->fs_armed = false;
     h->fspart_ctas = (size_t)cdiv(maxrows, 128) + 2 * (size_t)h->nsm + 8;
     if (cudaMalloc((void**)&h->fspart, sizeof(float) * tc::FS_PMAX * 128 * h->fspart_ctas) != cudaSuccess ||
@@ -1710,7 +1714,8 @@ frsvt_status frsvt_draw_omega(frsvt_handle* h, int64_t call, void* out, int64_t 
   h->fs_armed = false;  // h->Om is overwritten
   if (h->cfg.dtype == FRSVT_F32)
     omega_kernel<float><<<grid1d(h->n * h->l), 256, 0, h->st>>>((float*)h->Om, h->n, h->l, &h->dev->r, 0,
-                                                               h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n);
+                                                               h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n,
+                                                               0, nullptr, h->om_tf32);
   else
     omega_kernel<double><<<grid1d(h->n * h->l), 256, 0, h->st>>>((double*)h->Om, h->n, h->l, &h->dev->r, 0,
                                                                 h->cfg.seed, 1000u + (uint32_t)call, nullptr, h->n);

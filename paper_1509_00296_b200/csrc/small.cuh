@@ -40,12 +40,13 @@ __device__ __forceinline__ double philox_normal(uint64_t seed, uint32_t stream, 
 // only them and writes them behind the carried columns). pmax_dev (nullable,
 // adaptive rank prediction P:204-215): at most *pmax_dev fresh columns, the
 // rest zero (a zero sample is dropped by the rank reveal, so the basis has
-// r + p columns: the sketch width of Eq. (7)).
+// r + p columns: the sketch width of Eq. (7)). tf32 (fp32 only,
+// FRSVT_OPT_TF32_OMEGA): drawn entries rounded to tf32 (rna).
 template <typename T>
 __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __restrict__ r_dev,
                              int use_r, uint64_t seed, uint32_t stream,
                              const T* __restrict__ override_om, int64_t ldo, int front = 0,
-                             const int* __restrict__ pmax_dev = nullptr) {
+                             const int* __restrict__ pmax_dev = nullptr, int tf32 = 0) {
   const int r = use_r ? *r_dev : 0;
   const int p = pmax_dev ? min(l - r, max(*pmax_dev, 0)) : l - r;
   const int64_t total = n * (int64_t)l;
@@ -57,7 +58,12 @@ __global__ void omega_kernel(T* __restrict__ Om, int64_t n, int l, const int* __
     if (front ? (c < p) : (c >= r && c < r + p)) {
       const int src = front ? c : c - r;
       if (override_om) v = override_om[i + src * ldo];
-      else v = (T)philox_normal(seed, stream, (uint64_t)src * (uint64_t)n + (uint64_t)i);
+      else {
+        v = (T)philox_normal(seed, stream, (uint64_t)src * (uint64_t)n + (uint64_t)i);
+        if constexpr (sizeof(T) == 4) {  // FRSVT_OPT_TF32_OMEGA: rna to tf32
+          if (tf32) v = __uint_as_float((__float_as_uint((float)v) + 0x1000u) & 0xFFFFE000u);
+        }
+      }
     }
     Om[idx] = v;
   }

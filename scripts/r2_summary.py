@@ -120,7 +120,8 @@ def main(tag, rnd):
             us = fnum(d, "gpu__time_duration.sum") * 1e-3
             if k not in best or rd + wr > best[k]["bytes_per_launch"]:
                 best[k] = {"kernel": d.get("Kernel Name", "")[:80], "bytes_per_launch": rd + wr,
-                           "dram_read_bytes": rd, "dram_write_bytes": wr, "tensor_pipe_pct": tp,
+                           "dram_read_bytes": rd, "dram_write_bytes": wr,
+                           "tensor_pipe_pct": tp if tp == tp else None,
                            "ncu_us": us,
                            "source": "ncu --set full --clock-control none, gpurun_out/%s (the launch of this kind "
                                      "with the most DRAM bytes: a full pass); profiles/%s_ncu_full_summary_%s.txt"

@@ -120,7 +120,16 @@ def uniform_matrix(seed, stream, rows, cols, device="cpu", chunk=1 << 26):
     return out.view(cols, rows).t()
 
 
-def omega(seed, call, n, l, device="cpu"):
+def omega(seed, call, n, l, device="cpu", tf32=False):
     """Omega of FRSVT call `call`: n x l i.i.d. N(0,1), stream 1000+call,
-    column-major."""
-    return normal_matrix(seed, 1000 + call, n, l, device=device)
+    column-major. tf32=True: the draws as a
+    handle with FRSVT_OPT_TF32_OMEGA holds them (fp32, then rounded to tf32:
+    round to nearest with ties away, i.e. + 0x1000 and the low 13 mantissa
+    bits cleared), returned in fp64 (exactly representable)."""
+    om = normal_matrix(seed, 1000 + call, n, l, device=device)
+    if not tf32:
+        return om
+    bits = om.float().contiguous().view(torch.int32).to(torch.int64)
+    bits = ((bits + 0x1000) & 0xFFFFE000) & 0xFFFFFFFF
+    bits = torch.where(bits >= 1 << 31, bits - (1 << 32), bits).to(torch.int32)
+    return bits.view(torch.float32).double().reshape(om.shape)

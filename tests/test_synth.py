@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from synth import make_config, normal, omega, uniform
+from synth import SEED0, make_config, normal, omega, uniform
 from synth.philox import normal_matrix, philox4x32_10
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -85,3 +85,33 @@ def test_recipes_are_column_major_and_typed():
     assert d["D"].dtype == torch.float32 and d["D"].stride() == (1, 64)
     cfg, d = make_config("c1")
     assert d["A"].dtype == torch.float64 and d["A"].stride() == (1, 200)
+
+
+def _tf32_rna_reference(x32):
+    """nearest tf32 (10 explicit mantissa bits) of an fp32 value, ties away from
+    zero, found by comparing the two neighbouring candidates exactly in fp64"""
+    import math
+    if x32 == 0.0:
+        return 0.0
+    e = math.frexp(abs(x32))[1]          # |x| in [2^(e-1), 2^e)
+    q = 2.0 ** (e - 1 - 10)              # tf32 spacing in that binade
+    lo = math.floor(abs(x32) / q) * q
+    hi = lo + q
+    a = abs(x32)
+    r = hi if (a - lo) >= (hi - a) else lo
+    return math.copysign(r, x32)
+
+
+def test_omega_tf32_option_rounding():
+    """FRSVT_OPT_TF32_OMEGA draws (synth side): the fp32 draw rounded to the
+    nearest tf32 value with ties away (NEXT-4 TF32-exact Omega), checked against
+    a brute-force nearest-candidate search; entries exactly tf32."""
+    full = omega(SEED0, 3, 97, 7)
+    t = omega(SEED0, 3, 97, 7, tf32=True)
+    assert t.shape == full.shape and t.dtype == torch.float64
+    x32 = full.float()
+    assert int((t.float().view(torch.int32) & 0x1FFF).abs().max()) == 0
+    ref = torch.tensor([_tf32_rna_reference(float(v)) for v in x32.reshape(-1)], dtype=torch.float64)
+    assert torch.equal(t.reshape(-1), ref)
+    rel = ((t - x32.double()).abs() / x32.double().abs()).max().item()
+    assert rel <= 2.0 ** -11
