@@ -70,6 +70,17 @@ __host__ __device__ constexpr size_t chol_inv_smem_bytes() {
 // per-row ready signal: an mbarrier of count 1 per row (arrive = release,
 // try_wait = acquire at CTA scope); measured on B200 at l = 120: 63 us per
 // factor vs 70 us with st.release / ld.acquire flags (a fence per publish)
+// 1/x for a pivot x > tol (> 0, finite): rcp.approx seed (~2^-23) and two
+// Newton steps (~2^-46 -> below one ulp after the second), shorter on the
+// pivot chain than the IEEE division's slow-path-guarded sequence
+__device__ __forceinline__ double ci_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
 __device__ __forceinline__ void ci_flag_release(uint64_t* f) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(f))
                : "memory");
@@ -171,7 +182,7 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
   if (w == 0 && p > 0) {
 #pragma unroll
     for (int j = 0; j < TJ; ++j) M[L + 32 * j] = m[0][j];
-    if (L == 0) invp[0] = m[0][0] > tol ? 1.0 / m[0][0] : 0.0;
+    if (L == 0) invp[0] = m[0][0] > tol ? ci_rcp(m[0][0]) : 0.0;
     __syncwarp();
     if (L == 0) ci_flag_release(rdy);
   }
@@ -209,7 +220,7 @@ chol_inv_kernel(const double* __restrict__ G, int l, const int* __restrict__ r_d
 #pragma unroll
         for (int j = 0; j < TJ; ++j) {
           rn[L + 32 * j] = m[i][j];
-          if (L + 32 * j == k1) invp[k1] = m[i][j] > tol ? 1.0 / m[i][j] : 0.0;
+          if (L + 32 * j == k1) invp[k1] = m[i][j] > tol ? ci_rcp(m[i][j]) : 0.0;
         }
       }
       __syncwarp();
