@@ -505,6 +505,37 @@ def run_ours(args, ws, rank, local, dist):
         cpu = {"value": rate, "unit": META[args.config]["unit"], "cores": _oracle_threads(), "kind": "oracle",
                "sample": sample}
 
+    # c1 only: the same single-CTA call as independent c1-shaped problems, one
+    # per CTA across the GPU in one launch (frsvt_batched_apply_f64, Omega of
+    # call 0 shared): the throughput of the design when calls do not depend on
+    # each other. Reported beside the sequential-call value, not instead of it.
+    batched = None
+    if args.config == "c1" and rank == 0:
+        from synth import omega as _omega
+        nb = 4 * torch.cuda.get_device_properties(dev).multi_processor_count
+        Ab = torch.empty((nb, cfg.n, cfg.m), dtype=torch.float64, device=dev).transpose(1, 2)
+        Ab.copy_(W.inp.unsqueeze(0).expand(nb, -1, -1))
+        Omb = _omega(cfg.seed, 0, cfg.n, cfg.l).to(dev)
+        Xb = torch.empty((nb, cfg.n, cfg.m), dtype=torch.float64, device=dev).transpose(1, 2)
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 1)):
+                P.batched_apply(Ab, Omb, q=cfg.q, tau=W.tau, X=Xb, stream=stream)
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kb = max(args.steps, 1)
+        b0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(kb):
+                P.batched_apply(Ab, Omb, q=cfg.q, tau=W.tau, X=Xb, stream=stream)
+        b1.record(stream)
+        barrier()
+        bms = b0.elapsed_time(b1)
+        batched = {"value": nb * kb / (bms / 1e3), "unit": "calls/s", "calls_per_launch": nb, "launches": kb,
+                   "ms_per_launch": bms / kb,
+                   "what": "independent c1-shaped fp64 calls, one CTA each (frsvt_batched_apply_f64), Omega of call 0 "
+                           "shared; inputs resident in HBM"}
+        del Ab, Xb
+
     if rank != 0:
         return None
     kernel_names = {"AX": "tc_pass3_kernel<AX> (A X passes)", "AtQ": "tc_pass3_kernel<ATQ> (A^T Q passes)",
@@ -522,7 +553,8 @@ def run_ours(args, ws, rank, local, dist):
                          "unit_algorithmic_bytes": unit_bytes, "unit_gbs": unit_gbs, "unit_frac": unit_gbs / hbm_peak,
                          "per_pass_scope": ("one eager step right after the timed graph replays" if graph is not None
                                             else "all timed steps")},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            **({"batched": batched} if batched is not None else {})}
 
 
 def main():

@@ -127,6 +127,13 @@ frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l,
                                  int64_t lda, int64_t strideA, const float* Omega, int64_t ldo, int32_t wmode,
                                  double tau, const double* tau_batch, const double* w, float* X, int64_t ldx,
                                  int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream);
+/* The same for fp64 matrices (products, orthonormalisation and the small SVD
+ * in fp64): 8 ((m + n) l + l^2 + 192) + 8 m n bytes of shared memory
+ * <= 227 KB (e.g. BASELINE c1's 200 x 100, l = 10). */
+frsvt_status frsvt_batched_apply_f64(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const double* A,
+                                     int64_t lda, int64_t strideA, const double* Omega, int64_t ldo, int32_t wmode,
+                                     double tau, const double* tau_batch, const double* w, double* X, int64_t ldx,
+                                     int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream);
 
 /* Loopback process group of `nranks` (2..FRSVT_LOOPBACK_MAX) virtual ranks:
  * the row-sharded path on ONE device and in ONE process,

@@ -58,31 +58,32 @@ def _ld(x, rows, dtype, name):
 
 
 def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None, X=None):
-    """frsvt_batched_apply: X[b] = FRSVT(A[b]) for a batch of small fp32
-    matrices (one CTA each). A: (batch, m, n) CUDA fp32 with each matrix
-    column-major (A[b].stride() == (1, ld)); Omega: n x l column-major. tau: a
-    float or a (batch,) tensor; w: (l,) weights. X (optional): the output,
-    (batch, m, n) fp32 with column-major matrices (any ld >= m, any batch
-    stride); allocated when None. Returns X, r (batch,) int32, sigma (batch, l)
-    float64."""
-    if A.dim() != 3 or A.dtype != torch.float32 or A.device.type != "cuda":
-        raise ValueError("A must be a (batch, m, n) CUDA fp32 tensor")
+    """frsvt_batched_apply (fp32) / frsvt_batched_apply_f64 (fp64): X[b] =
+    FRSVT(A[b]) for a batch of small matrices (one CTA each). A: (batch, m, n)
+    CUDA fp32 or fp64 with each matrix column-major (A[b].stride() == (1, ld));
+    Omega: n x l column-major. tau: a float or a (batch,) tensor; w: (l,)
+    weights. X (optional): the output, (batch, m, n) of A's dtype with
+    column-major matrices (any ld >= m, any batch stride); allocated when None.
+    Returns X, r (batch,) int32, sigma (batch, l) float64."""
+    if A.dim() != 3 or A.dtype not in (torch.float32, torch.float64) or A.device.type != "cuda":
+        raise ValueError("A must be a (batch, m, n) CUDA fp32 or fp64 tensor")
+    dt = A.dtype
     batch, m, n = A.shape
     if batch == 0:
         l = Omega.shape[1]
-        return (torch.empty((0, m, n), dtype=torch.float32, device=A.device),
+        return (torch.empty((0, m, n), dtype=dt, device=A.device),
                 torch.empty(0, dtype=torch.int32, device=A.device),
                 torch.empty((0, l), dtype=torch.float64, device=A.device))
     if A.stride(1) != 1:
         raise ValueError("each A[b] must be column-major")
     lda, sA = A.stride(2), A.stride(0)
-    Om = colmajor(Omega.to(device=A.device, dtype=torch.float32))
+    Om = colmajor(Omega.to(device=A.device, dtype=dt))
     l = Om.shape[1]
     if X is None:
-        X = torch.empty((batch, n, m), dtype=torch.float32, device=A.device).transpose(1, 2)
-    elif (X.shape != A.shape or X.dtype != torch.float32 or X.device != A.device or X.stride(1) != 1
+        X = torch.empty((batch, n, m), dtype=dt, device=A.device).transpose(1, 2)
+    elif (X.shape != A.shape or X.dtype != dt or X.device != A.device or X.stride(1) != 1
           or X.stride(2) < max(1, m)):
-        raise ValueError("X must be a (batch, m, n) fp32 tensor on A's device with column-major matrices")
+        raise ValueError("X must be a (batch, m, n) tensor of A's dtype on A's device with column-major matrices")
     r = torch.empty(batch, dtype=torch.int32, device=A.device)
     sig = torch.empty((batch, l), dtype=torch.float64, device=A.device)
     wmode, tau_s, tau_p, w_p = 0, 0.0, None, None
@@ -98,7 +99,8 @@ def batched_apply(A, Omega, q=1, tau=None, w=None, stream=None, X=None):
     st = stream if stream is not None else torch.cuda.current_stream()
     for t in (A, Om, X) + ((wt,) if w is not None else ()) + ((tt,) if tau_p is not None else ()):
         t.record_stream(st)  # kept alive for the asynchronous kernel on `st`
-    _check("frsvt_batched_apply", lib.frsvt_batched_apply(
+    name = "frsvt_batched_apply" if dt == torch.float32 else "frsvt_batched_apply_f64"
+    _check(name, getattr(lib, name)(
         int(batch), int(m), int(n), int(l), int(q), ctypes.c_void_p(A.data_ptr()), int(lda), int(sA),
         ctypes.c_void_p(Om.data_ptr()), int(Om.stride(1)), wmode, tau_s, tau_p, w_p, ctypes.c_void_p(X.data_ptr()),
         int(X.stride(2)), int(X.stride(0)), ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(sig.data_ptr()),

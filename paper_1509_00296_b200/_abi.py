@@ -10,7 +10,7 @@ LIB_PATH = os.path.join(_HERE, "libfrsvt.so")
 
 # every entry point include/frsvt.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
-    "frsvt_batched_apply", "frsvt_loopback_create", "frsvt_loopback_destroy", "frsvt_get_unique_id", "frsvt_create", "frsvt_destroy", "frsvt_status_string",
+    "frsvt_batched_apply", "frsvt_batched_apply_f64", "frsvt_loopback_create", "frsvt_loopback_destroy", "frsvt_get_unique_id", "frsvt_create", "frsvt_destroy", "frsvt_status_string",
     "frsvt_apply", "frsvt_apply_weighted", "rpca_alm_step", "frsvt_set_omega",
     "frsvt_draw_omega", "frsvt_get_carry", "frsvt_set_carry", "frsvt_reset_carry",
     "frsvt_set_call_index", "frsvt_set_adaptive_rank", "frsvt_get_info", "rpca_get_mu", "rpca_set_mu",
@@ -57,6 +57,8 @@ def load_library(path=LIB_PATH):
     sig = {
         "frsvt_batched_apply": (i32, [i32, i64, i64, i32, i32, vp, i64, i64, vp, i64, i32, dbl, vp, vp, vp, i64, i64,
                                       vp, vp, vp]),
+        "frsvt_batched_apply_f64": (i32, [i32, i64, i64, i32, i32, vp, i64, i64, vp, i64, i32, dbl, vp, vp, vp, i64,
+                                          i64, vp, vp, vp]),
         "frsvt_loopback_create": (i32, [i32, P(vp)]),
         "frsvt_loopback_destroy": (None, [vp]),
         "frsvt_get_unique_id": (i32, [P(ctypes.c_ubyte)]),

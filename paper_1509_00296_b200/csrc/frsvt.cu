@@ -1371,25 +1371,12 @@ static bool rank_uniform_layout(const frsvt_handle* h, const void* A, int64_t ld
 }
 
 // ============================================================== C ABI
-extern "C" {
-
-const char* frsvt_status_string(frsvt_status s) {
-  switch (s) {
-    case FRSVT_OK: return "ok";
-    case FRSVT_EINVAL: return "invalid argument";
-    case FRSVT_ENOCONV: return "Jacobi sweep cap reached";
-    case FRSVT_ECUDA: return "CUDA error";
-    case FRSVT_ENCCL: return "NCCL error";
-    case FRSVT_ENONFINITE: return "non-finite value reached a Gram diagonal";
-    case FRSVT_ENOMEM: return "out of device memory";
-  }
-  return "unknown status";
-}
-
-frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const float* A,
-                                 int64_t lda, int64_t strideA, const float* Omega, int64_t ldo, int32_t wmode,
-                                 double tau, const double* tau_batch, const double* w, float* X, int64_t ldx,
-                                 int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream) {
+// frsvt_batched_apply / _f64: validation and one launch of the one-CTA kernel
+template <typename T>
+static frsvt_status batched_apply_t(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const T* A, int64_t lda,
+                                    int64_t strideA, const T* Omega, int64_t ldo, int32_t wmode, double tau,
+                                    const double* tau_batch, const double* w, T* X, int64_t ldx, int64_t strideX,
+                                    int32_t* r_out, double* sigma_out, void* cuda_stream) {
   if (batch < 0 || m < 1 || n < 1 || l < 1 || l > BT_LMAX || l > m || l > n || q < 0 || q > 16) return FRSVT_EINVAL;
   if (lda < m || ldx < m || ldo < n || strideA < lda * n || strideX < ldx * n) return FRSVT_EINVAL;
   if (batch == 0) return FRSVT_OK;  // nothing to do (the pointers may be NULL)
@@ -1401,9 +1388,9 @@ frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l,
   } else {
     return FRSVT_EINVAL;
   }
-  if (!bt_fits(m, n, l, 4)) return FRSVT_EINVAL;
+  if (!bt_fits(m, n, l, (int)sizeof(T))) return FRSVT_EINVAL;
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  CK(bt_set_attrs<float>());
+  CK(bt_set_attrs<T>());
   BtArgs a{};
   a.m = (int)m;
   a.n = (int)n;
@@ -1423,8 +1410,39 @@ frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l,
   a.strideX = strideX;
   a.r_b = r_out;
   a.sig_b = sigma_out;
-  CK(bt_launch<float>(a, batch, st));
+  CK(bt_launch<T>(a, batch, st));
   return FRSVT_OK;
+}
+
+extern "C" {
+
+const char* frsvt_status_string(frsvt_status s) {
+  switch (s) {
+    case FRSVT_OK: return "ok";
+    case FRSVT_EINVAL: return "invalid argument";
+    case FRSVT_ENOCONV: return "Jacobi sweep cap reached";
+    case FRSVT_ECUDA: return "CUDA error";
+    case FRSVT_ENCCL: return "NCCL error";
+    case FRSVT_ENONFINITE: return "non-finite value reached a Gram diagonal";
+    case FRSVT_ENOMEM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+frsvt_status frsvt_batched_apply(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const float* A,
+                                 int64_t lda, int64_t strideA, const float* Omega, int64_t ldo, int32_t wmode,
+                                 double tau, const double* tau_batch, const double* w, float* X, int64_t ldx,
+                                 int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream) {
+  return batched_apply_t<float>(batch, m, n, l, q, A, lda, strideA, Omega, ldo, wmode, tau, tau_batch, w, X, ldx,
+                                strideX, r_out, sigma_out, cuda_stream);
+}
+
+frsvt_status frsvt_batched_apply_f64(int32_t batch, int64_t m, int64_t n, int32_t l, int32_t q, const double* A,
+                                     int64_t lda, int64_t strideA, const double* Omega, int64_t ldo, int32_t wmode,
+                                     double tau, const double* tau_batch, const double* w, double* X, int64_t ldx,
+                                     int64_t strideX, int32_t* r_out, double* sigma_out, void* cuda_stream) {
+  return batched_apply_t<double>(batch, m, n, l, q, A, lda, strideA, Omega, ldo, wmode, tau, tau_batch, w, X, ldx,
+                                 strideX, r_out, sigma_out, cuda_stream);
 }
 
 frsvt_status frsvt_loopback_create(int32_t nranks, frsvt_group** out) {

@@ -71,3 +71,24 @@ def test_batched_weighted_and_empty(P):
         assert int(r[b]) == ref.r
     Xe, re, _ = P.batched_apply(_dev(A[:0]), torch.from_numpy(Om), q=1, tau=1.0)
     assert Xe.shape[0] == 0 and re.shape[0] == 0
+
+
+@pytest.mark.parametrize("B,m,n,l,q,rank", [(20, 200, 100, 10, 1, 5), (7, 37, 29, 8, 2, 3)])
+def test_batched_fp64_against_oracle(P, B, m, n, l, q, rank):
+    """frsvt_batched_apply_f64: BASELINE c1-shaped fp64 matrices (200 x 100,
+    l = 10, q = 1) in one launch, each within the fp64 bar (Z14 <= 1e-10)."""
+    rng = np.random.default_rng(B + m)
+    A = np.stack([rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n))
+                  + 0.01 * rng.standard_normal((m, n)) for _ in range(B)])
+    Om = omega(79, 0, n, l).numpy()
+    taus = np.array([0.5 * np.linalg.svd(a, compute_uv=False)[rank - 1] for a in A])
+    Ad = torch.from_numpy(np.ascontiguousarray(A.transpose(0, 2, 1))).cuda().transpose(1, 2)
+    X, r, sig = P.batched_apply(Ad, torch.from_numpy(Om), q=q, tau=torch.from_numpy(taus))
+    torch.cuda.synchronize()
+    assert X.dtype == torch.float64
+    X, r, sig = X.cpu().numpy(), r.cpu().numpy(), sig.cpu().numpy()
+    for b in range(B):
+        ref = oracle.frsvt(A[b], Om, l, q, tau=taus[b], rp=False)
+        assert z14(X[b], ref.X, A[b]) <= 1e-10, b
+        assert r[b] == ref.r, b
+        assert np.allclose(sig[b, : ref.r], ref.sigma[: ref.r], rtol=1e-11), b
